@@ -1,0 +1,168 @@
+/*
+ * qsim.h -- C-ABI of the B200-native (sm_100a) FP64 state-vector engine for the
+ * QAOA / AQA hot path of arXiv:2104.03293 ("GPU-accelerated simulations of quantum
+ * annealing and the quantum approximate optimization algorithm", JUQCS-G).
+ *
+ * Citations "P:<line>" refer to the paper's LaTeX source, equation labels
+ * are the paper's (eq:HC, eq:QAOA_state, eq:beta_k, eq:gamma_k, ...).
+ *
+ * Conventions shared by every call (readings R1-R4):
+ *   - n qubits; basis label z in [0, 2^n); qubit j <-> bit j of z (little endian).
+ *   - spin s_j(z) = 2 bit_j(z) - 1: |0> is the -1 and |1> the +1 eigenstate of
+ *     sigma^z_j.
+ *   - H_C = sum_i h_i sigma^z_i + sum_{i<j} J_ij sigma^z_i sigma^z_j (eq:HC):
+ *     E(z) = sum_i h_i s_i + sum_{i<j} J_ij s_i s_j.  The constant C of eq:HCC is not
+ *     part of H_C (global phase) and never enters any result.
+ *   - H_D = sum_i sigma^x_i.
+ *   - amplitudes are complex128, passed as interleaved (re, im) doubles.
+ *
+ * Ownership and threading:
+ *   - a qsim_t* is owned by the caller from create until destroy; all pointer
+ *     arguments are host pointers unless stated otherwise, read (or written) during
+ *     the call only, never retained.
+ *   - single writer per handle: calls on one handle must not run concurrently.
+ *   - qsim_apply_* and qsim_init_plus enqueue work on the handle's CUDA stream and
+ *     may return before it completes; calls that return values to the host
+ *     (expect_hc, norm2, success_prob, get_amplitudes, energies, sync) synchronise.
+ *   - multi-GPU handles (world > 1) are SPMD collectives: every rank makes the same
+ *     calls with the same arguments, and scalar / gathered results are returned on
+ *     every rank.
+ *
+ * Errors: every int-returning call returns QSIM_OK (0) or a negative QSIM_E* code;
+ * qsim_last_error() describes the most recent failure on that handle.  A call that
+ * fails with QSIM_EINVAL / QSIM_ERANGE / QSIM_ESTATE leaves the state unchanged.
+ * QSIM_ECUDA / QSIM_ENCCL leave the handle unusable except for destroy.
+ */
+#ifndef QSIM_H
+#define QSIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qsim qsim_t; /* opaque */
+
+enum {
+    QSIM_OK = 0,
+    QSIM_EINVAL = -1,      /* bad argument: NULL pointer, NaN/Inf, p < 1, n out of range */
+    QSIM_ENOMEM = -2,      /* device memory capacity exceeded for 2^n amplitudes */
+    QSIM_ERANGE = -3,      /* basis index out of [0, 2^n) */
+    QSIM_ESTATE = -4,      /* qsim_set_ising not called yet */
+    QSIM_EUNSUPPORTED = -5,/* precision other than QSIM_FP64, or layout not supported */
+    QSIM_ECUDA = -6,       /* CUDA runtime error (message in qsim_last_error) */
+    QSIM_ENCCL = -7        /* NCCL error (multi-GPU handles) */
+};
+
+enum { QSIM_FP64 = 0, QSIM_FP32 = 1 /* reserved; returns QSIM_EUNSUPPORTED */ };
+
+/* Create a single-GPU handle on the current CUDA device for an n-qubit state
+ * (1 <= n <= 40; the library allocates 16 * 2^n bytes of device memory, QSIM_ENOMEM
+ * if that fails).  The state starts as |+>^n.  precision must be QSIM_FP64. */
+int qsim_create(int n, int precision, qsim_t **out);
+
+/* Multi-GPU / embedding variant.  The state is partitioned over `world` = 2^g ranks
+ * on its top g physical qubits (the "global" qubits): rank r holds the
+ * 2^(n-g) amplitudes whose global bits equal r.  `nccl_unique_id` points to the 128
+ * bytes of an ncclUniqueId created on rank 0 and broadcast to all ranks (ignored
+ * when world == 1).  `state_buf` (device pointer, optional) provides caller-owned
+ * storage of buf_bytes >= 16 * 2^(n-g) bytes (the library then does not allocate
+ * the state); `cuda_stream` (cudaStream_t, optional) is the stream all work is
+ * enqueued on.  world must be a power of two <= 8 with n - g >= 13. */
+int qsim_create_ex(int n, int precision, int rank, int world, const void *nccl_unique_id,
+                   void *state_buf, size_t buf_bytes, void *cuda_stream, qsim_t **out);
+
+int qsim_destroy(qsim_t *q);
+
+/* Upload the Ising problem (eq:HC): h[n] and J[n*n] row-major, of which only the
+ * entries with i < j are read.  Values must be finite (QSIM_EINVAL otherwise).
+ * E(z) is bit-exact when every h_i, J_ij is a multiple of 2^-m with
+ * sum |coef| 2^m < 2^53 (dyadic data such as the paper's half-integer exact-cover
+ * fields); other data is accepted without the bit-exactness claim. */
+int qsim_set_ising(qsim_t *q, const double *h, const double *J);
+
+/* Reset the state to |+>^n: psi_z = 2^(-n/2).  Applied lazily: the
+ * first pass of the next qsim_apply_* writes it instead of reading the state. */
+int qsim_init_plus(qsim_t *q);
+
+/* Apply p QAOA layers to the current state (eq:QAOA_state, with the order
+ * of Appendix A): for k = 1..p, psi <- e^{-i beta_k H_D} e^{-i gamma_k H_C} psi,
+ * i.e. the cost phase psi_z <- e^{-i gamma_k E(z)} psi_z followed by the mixer
+ * e^{-i beta_k sigma^x} on every qubit ("rotations around the x axis with angle
+ * 2 beta_k").  gamma[p], beta[p] are used as given (never reduced modulo
+ * pi / 2 pi).  p >= 1. */
+int qsim_apply_qaoa(qsim_t *q, const double *gamma, const double *beta, int p);
+
+/* AQA / second-order QAOA initialisation (eq:beta_k, eq:gamma_k,
+ * P:338-347): tau = T/p (t_anneal = (n_steps + 1) tau = T), s_k = (k-1)/(p-1)
+ * for k = 1..p (== k'/n_steps, k' = 0..n_steps, n_steps = p-1), A and B piecewise
+ * linear through the n_knots knots (s[0] = 0 < ... < s[n_knots-1] = 1),
+ *   beta_k = -tau (A(s_{k+1}) + A(s_k)) / 2 (k < p),  beta_p = -tau A(s_p) / 2,
+ *   gamma_k = tau B(s_k),
+ * then exactly qsim_apply_qaoa(gamma, beta, p).  A, B are in angular units per unit
+ * of T (no 2 pi applied; reading R7).  p >= 2 (reading R8). */
+int qsim_apply_aqa(qsim_t *q, double T, int p, const double *s, const double *A, const double *B,
+                   int n_knots);
+
+/* Host-only helper (no device work): the angles qsim_apply_aqa uses. */
+int qsim_aqa_angles(double T, int p, const double *s, const double *A, const double *B,
+                    int n_knots, double *gamma_out, double *beta_out);
+
+/* <H_C> = sum_z |psi_z|^2 E(z) (E_p(beta, gamma)), constant C excluded. */
+int qsim_expect_hc(qsim_t *q, double *out);
+
+/* ||psi||^2 = sum_z |psi_z|^2. */
+int qsim_norm2(qsim_t *q, double *out);
+
+/* Success probability sum_{z in ground_states} |psi_z|^2.  count >= 1,
+ * every label < 2^n (QSIM_ERANGE otherwise). */
+int qsim_success_prob(qsim_t *q, const uint64_t *ground_states, int count, double *out);
+
+/* Copy amplitudes psi_z for z = first .. first+count-1 in LOGICAL order (any qubit
+ * relabelling done by the multi-GPU engine is undone) to out[2*count]. */
+int qsim_get_amplitudes(qsim_t *q, uint64_t first, uint64_t count, double *out);
+
+/* Test / diagnostic: E(z) for z = first .. first+count-1, computed on the device with
+ * the same tile-factorised energy arithmetic the cost-phase kernel uses. */
+int qsim_energies(qsim_t *q, uint64_t first, uint64_t count, double *out);
+
+/* Wait for all work enqueued on the handle's stream. */
+int qsim_sync(qsim_t *q);
+
+/* Host-only planner introspection (no device work): for an n-qubit state on `world`
+ * GPUs and p layers, the number of full HBM passes over the local shard and of
+ * global-qubit swaps one qsim_apply_qaoa performs, and the amplitudes each rank
+ * sends per swap.  Returns QSIM_EINVAL for unsupported layouts. */
+int qsim_plan_counts(int n, int world, int p, int *passes_out, int *swaps_out,
+                     uint64_t *amps_sent_per_swap_out);
+
+/* Host-only: the physical bit positions of the qubits after `layers` swaps of the
+ * multi-GPU schedule (pos_out[q] = physical position of logical qubit q). */
+int qsim_plan_positions(int n, int world, int layers, int *pos_out);
+
+/* Multi-GPU bootstrap helper: write a fresh ncclUniqueId (128 bytes) to out128 (call on
+ * rank 0, broadcast the bytes, pass them to qsim_create_ex on every rank). */
+int qsim_nccl_unique_id(void *out128);
+
+/* Diagnostics for benchmarking: when enabled, every tile-pass kernel launch is bracketed
+ * by CUDA events on the handle's stream.  qsim_profile_read synchronises and returns the
+ * summed pass-kernel time (ms), the number of pass launches and their summed algorithmic
+ * HBM bytes (32 B per amplitude read+written, 16 B for the write-only init pass) since the
+ * last enable/read, then resets the counters. */
+int qsim_profile_enable(qsim_t *q, int on);
+int qsim_profile_read(qsim_t *q, double *ms_sum, uint64_t *count, double *bytes_sum);
+
+/* Number of kernels the library has launched on this handle (for bench reporting). */
+uint64_t qsim_kernel_launches(const qsim_t *q);
+
+/* Message for the last error on q (or for the last failed create when q is NULL). */
+const char *qsim_last_error(const qsim_t *q);
+
+const char *qsim_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QSIM_H */

@@ -1,0 +1,78 @@
+// qsim_device.h -- parameter blocks and launchers shared by the engine (qsim_engine.cu)
+// and the kernels (qsim_device.cu).  Plain structs; no device code.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace qk {
+
+typedef unsigned long long u64;
+constexpr int KT = 12;          // tile bits per pass
+constexpr int TILE = 1 << KT;   // amplitudes per tile
+constexpr int NTHR = 256;       // threads per CTA
+constexpr int NR = 16;          // amplitudes per thread
+constexpr int NMAX = 40;        // max qubits
+constexpr int SM_TILE_BYTES = TILE * 16;
+
+struct Mix {
+    double t;   // tan(beta) (form 0) or -cot(beta) (form 1)
+    int form;
+};
+
+struct PassParams {
+    double2 *psi;        // local shard, 2^m amplitudes
+    const double *hp;    // physical-frame fields, n
+    const double *Jp;    // physical-frame couplings, n*n symmetric, zero diagonal
+    int n, m;
+    u64 xglob;           // global (rank) bits placed at positions m..n-1
+    u64 lmask;           // mask of the tile-bit positions
+    int L[KT];           // tile-bit positions (ascending)
+    int nseg;            // complement segments: tile id bits -> physical positions
+    int seg_len[8];
+    int seg_dst[8];
+    u64 ntiles;
+    unsigned mix1, mix2; // tile-bit masks mixed before / after the phase
+    Mix c1, c2;
+    double2 scale;       // kappa1^|mix1| * kappa2^|mix2|
+    int init, phase, reduce;
+    double a0;           // 2^(-n/2)
+    double gamma;
+    double *part;        // reduce partials, 2 per CTA
+};
+
+struct SmallParams {
+    double2 *psi;
+    const double *hp, *Jp;
+    const double *ang;   // gamma[p], beta[p]
+    int n, p, init, reduce;
+    double a0;
+    double *res;         // 2 doubles
+};
+
+struct GatherParams {
+    int n, m;
+    u64 rank;
+    u64 first, count;
+    const u64 *list;     // optional explicit logical labels (device)
+    unsigned char pos[NMAX];
+};
+
+struct ProbeSet {
+    int L[KT];
+    int k;
+    u64 lmask;
+};
+
+size_t pass_smem_bytes();
+cudaError_t setup_kernels();
+cudaError_t launch_pass(const PassParams &P, int grid, cudaStream_t s);
+cudaError_t launch_reduce(const PassParams &P, int grid, cudaStream_t s);
+cudaError_t launch_sum_partials(const double *part, int nparts, double *res, cudaStream_t s);
+cudaError_t launch_small(const SmallParams &P, cudaStream_t s);
+cudaError_t launch_init_plus(double2 *psi, u64 count, double a0, int grid, cudaStream_t s);
+cudaError_t launch_gather(const GatherParams &G, const double2 *psi, double2 *out, int grid, cudaStream_t s);
+cudaError_t launch_energy_probe(const GatherParams &G, const double *hp, const double *Jp,
+                                const ProbeSet &S, double *out, int grid, cudaStream_t s);
+
+}  // namespace qk

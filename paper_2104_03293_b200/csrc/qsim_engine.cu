@@ -1,0 +1,829 @@
+// qsim_engine.cu -- host engine and C-ABI (include/qsim.h) of the B200-native QAOA/AQA
+// state-vector engine (arXiv:2104.03293).
+//
+//  * pass planner: tile sets over the local bits, boustrophedon layer order on one GPU
+//    ((P-1) p + 1 HBM passes for p layers), fixed global-qubit swap
+//    schedule on G > 1 GPUs (P p + 1 passes, one swap per layer),
+//  * angle generation for AQA (eq:beta_k / eq:gamma_k),
+//  * permutation bookkeeping (the paper's "local permutation array"),
+//  * NCCL all-to-all qubit swap and all-reduce of the reduction scalars.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/qsim.h"
+#include "qsim_device.h"
+
+using qk::u64;
+
+namespace {
+
+std::string g_create_error;
+
+struct TileSet {
+    int L[qk::KT];
+    u64 lmask;
+    unsigned own;  // tile-bit mask of the bits this set mixes
+    int nseg;
+    int seg_len[8], seg_dst[8];
+    u64 ntiles;
+};
+
+struct PassOp {
+    int set;
+    bool init, phase, reduce;
+    unsigned mix1, mix2;
+    double b1, b2, gamma;
+    bool swap_after;  // multi-GPU: global-qubit swap after this pass
+};
+
+TileSet make_set(int m, const std::vector<int> &Lpos, unsigned own) {
+    TileSet S{};
+    u64 lm = 0;
+    for (int i = 0; i < qk::KT; ++i) {
+        S.L[i] = Lpos[i];
+        lm |= 1ull << Lpos[i];
+    }
+    S.lmask = lm;
+    S.own = own;
+    int ns = 0, p = 0;
+    while (p < m) {
+        if ((lm >> p) & 1ull) { ++p; continue; }
+        int a = p;
+        while (p < m && !((lm >> p) & 1ull)) ++p;
+        S.seg_dst[ns] = a;
+        S.seg_len[ns] = p - a;
+        ++ns;
+    }
+    S.nseg = ns;
+    S.ntiles = 1ull << (m - qk::KT);
+    return S;
+}
+
+// Tile sets over m >= 13 local bits: S_0 = bits 0..11 (all mixed); then runs of <= 9
+// mixed bits taken top-down from bit m-1, each completed to 12 tile bits with the
+// lowest bits as unmixed "passengers" (>= 3 of them -> >= 128-byte coalesced runs).
+std::vector<TileSet> build_sets(int m) {
+    std::vector<std::pair<int, int>> runs;  // [a, a+len)
+    int end = m;
+    while (end > qk::KT) {
+        int len = std::min(9, end - qk::KT);
+        runs.push_back({end - len, len});
+        end -= len;
+    }
+    std::reverse(runs.begin(), runs.end());
+    std::vector<TileSet> sets;
+    std::vector<int> L0(qk::KT);
+    for (int i = 0; i < qk::KT; ++i) L0[i] = i;
+    sets.push_back(make_set(m, L0, (1u << qk::KT) - 1));
+    for (auto &r : runs) {
+        std::vector<int> L;
+        int npass = qk::KT - r.second;
+        for (int i = 0; i < npass; ++i) L.push_back(i);
+        for (int i = 0; i < r.second; ++i) L.push_back(r.first + i);
+        sets.push_back(make_set(m, L, ((1u << r.second) - 1) << npass));
+    }
+    return sets;
+}
+
+// pass schedule for p layers (see file header); `first_init` fuses |+>^n into pass 0
+std::vector<PassOp> build_schedule(int nsets, int g, int p, const double *gam, const double *bet,
+                                   bool first_init) {
+    std::vector<PassOp> ops;
+    const int P = nsets;
+    if (g == 0) {
+        auto seq = [&](int k, int idx) { return (k % 2 == 0) ? idx : P - 1 - idx; };
+        ops.push_back({seq(0, 0), first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false});
+        for (int k = 0; k < p; ++k) {
+            for (int idx = 1; idx < P; ++idx) {
+                int s = seq(k, idx);
+                if (idx == P - 1 && k < p - 1)
+                    ops.push_back({s, false, true, false, ~0u, ~0u, bet[k], bet[k + 1], gam[k + 1], false});
+                else
+                    ops.push_back({s, false, false, false, ~0u, 0u, bet[k], 0.0, 0.0, false});
+            }
+        }
+    } else {
+        const int top = P - 1;
+        const unsigned arrivals = ((1u << g) - 1) << (qk::KT - g);  // top g tile bits of the top set
+        ops.push_back({top, first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false});
+        for (int k = 0; k < p; ++k) {
+            for (int s = P - 2; s >= 0; --s) ops.push_back({s, false, false, false, ~0u, 0u, bet[k], 0.0, 0.0, false});
+            ops.back().swap_after = true;
+            if (k < p - 1)
+                ops.push_back({top, false, true, false, arrivals, ~0u, bet[k], bet[k + 1], gam[k + 1], false});
+            else
+                ops.push_back({top, false, false, false, arrivals, 0u, bet[k], 0.0, 0.0, false});
+        }
+    }
+    ops.back().reduce = true;
+    return ops;
+}
+
+// e^{-i b X} = kappa * (scaled butterfly):  form 0 kappa = cos b, t = tan b; form 1
+// kappa = -i sin b, t = -cot b (|tan b| > 1).  Exact 2x2 unitary either way.
+qk::Mix mix_coef(double b, std::complex<double> &kappa) {
+    double s = std::sin(b), c = std::cos(b);
+    qk::Mix mx;
+    if (std::fabs(c) >= std::fabs(s)) {
+        mx.form = 0;
+        mx.t = s / c;
+        kappa = {c, 0.0};
+    } else {
+        mx.form = 1;
+        mx.t = -c / s;
+        kappa = {0.0, -s};
+    }
+    return mx;
+}
+
+std::complex<double> cpow_int(std::complex<double> z, int e) {
+    std::complex<double> r(1.0, 0.0);
+    for (int i = 0; i < e; ++i) r *= z;
+    return r;
+}
+
+double pwl(const double *ks, const double *kv, int m, double s) {
+    if (s <= ks[0]) return kv[0];
+    for (int j = 0; j + 1 < m; ++j)
+        if (s <= ks[j + 1]) return kv[j] + (kv[j + 1] - kv[j]) * (s - ks[j]) / (ks[j + 1] - ks[j]);
+    return kv[m - 1];
+}
+
+int ilog2(int w) {
+    int g = 0;
+    while ((1 << g) < w) ++g;
+    return (1 << g) == w ? g : -1;
+}
+
+}  // namespace
+
+struct qsim {
+    int n = 0, m = 0, g = 0, rank = 0, world = 1;
+    int dev = 0, num_sms = 148;
+    double2 *psi = nullptr;
+    bool own_psi = false;
+    double2 *tmp = nullptr;  // swap buffer (multi-GPU, when memory allows)
+    void *user_buf = nullptr; // caller-owned state storage (never freed here)
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    bool has_ising = false;
+    std::vector<double> h, J;  // logical, J symmetric with zero diagonal
+    int parity = 0;            // number of swaps mod 2 (permutation state)
+    double *d_hp[2] = {nullptr, nullptr}, *d_Jp[2] = {nullptr, nullptr};
+    double *d_part = nullptr, *d_res = nullptr, *d_ang = nullptr;
+    size_t ang_cap = 0;
+    void *d_scratch = nullptr;
+    size_t scratch_cap = 0;
+    std::vector<TileSet> sets;
+    bool pending_plus = true;
+    bool res_valid = false;
+    uint64_t launches = 0;
+    std::string err;
+    // optional per-pass timing (CUDA events on the handle's stream around each pass launch)
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<double> prof_bytes;  // algorithmic bytes of each recorded pass
+};
+
+namespace {
+
+int fail(qsim *q, int code, const std::string &msg) {
+    if (q) q->err = msg;
+    else g_create_error = msg;
+    return code;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(q, QSIM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+    } while (0)
+
+#define NK(call)                                                                              \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return fail(q, QSIM_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));   \
+    } while (0)
+
+int grid_for(const qsim *q, u64 ntiles) {
+    u64 g = (u64)q->num_sms * 2;
+    return (int)std::min<u64>(g, ntiles);
+}
+
+// physical position of logical qubit qb in permutation state `par`
+int phys_pos(int n, int m, int g, int par, int qb) {
+    if (!par || g == 0) return qb;
+    if (qb >= m - g && qb < m) return qb + g;  // top local <-> global
+    if (qb >= m) return qb - g;
+    return qb;
+}
+
+int scratch(qsim *q, size_t bytes) {
+    if (q->scratch_cap >= bytes) return QSIM_OK;
+    if (q->d_scratch) cudaFree(q->d_scratch);
+    q->d_scratch = nullptr;
+    q->scratch_cap = 0;
+    CK(cudaMalloc(&q->d_scratch, bytes));
+    q->scratch_cap = bytes;
+    return QSIM_OK;
+}
+
+int materialize_plus(qsim *q) {
+    if (!q->pending_plus) return QSIM_OK;
+    double a0 = std::pow(2.0, -0.5 * q->n);
+    CK(qk::launch_init_plus(q->psi, 1ull << q->m, a0, q->num_sms * 8, q->st));
+    q->launches++;
+    q->pending_plus = false;
+    q->res_valid = false;
+    return QSIM_OK;
+}
+
+qk::PassParams base_params(qsim *q, const TileSet &S) {
+    qk::PassParams P{};
+    P.psi = q->psi;
+    P.hp = q->d_hp[q->parity];
+    P.Jp = q->d_Jp[q->parity];
+    P.n = q->n;
+    P.m = q->m;
+    P.xglob = (u64)q->rank << q->m;
+    P.lmask = S.lmask;
+    for (int i = 0; i < qk::KT; ++i) P.L[i] = S.L[i];
+    P.nseg = S.nseg;
+    for (int i = 0; i < 8; ++i) {
+        P.seg_len[i] = S.seg_len[i];
+        P.seg_dst[i] = S.seg_dst[i];
+    }
+    P.ntiles = S.ntiles;
+    P.a0 = std::pow(2.0, -0.5 * q->n);
+    P.part = q->d_part;
+    P.scale = make_double2(1.0, 0.0);
+    return P;
+}
+
+int finish_reduce(qsim *q, int nparts) {
+    CK(qk::launch_sum_partials(q->d_part, nparts, q->d_res, q->st));
+    q->launches++;
+    if (q->world > 1) NK(ncclAllReduce(q->d_res, q->d_res, 2, ncclDouble, ncclSum, q->comm, q->st));
+    q->res_valid = true;
+    return QSIM_OK;
+}
+
+// global-qubit swap: positions [m-g, m) <-> [m, n); rank r's chunk c <-> rank c's chunk r
+int do_swap(qsim *q) {
+    const int G = q->world;
+    const u64 chunk = 1ull << (q->m - q->g);  // amplitudes per chunk
+    const size_t cbytes = chunk * sizeof(double2);
+    if (q->tmp) {
+        NK(ncclGroupStart());
+        for (int c = 0; c < G; ++c) {
+            if (c == q->rank) continue;
+            NK(ncclSend(q->psi + c * chunk, chunk * 2, ncclDouble, c, q->comm, q->st));
+            NK(ncclRecv(q->tmp + c * chunk, chunk * 2, ncclDouble, c, q->comm, q->st));
+        }
+        NK(ncclGroupEnd());
+        CK(cudaMemcpyAsync(q->tmp + q->rank * chunk, q->psi + q->rank * chunk, cbytes,
+                           cudaMemcpyDeviceToDevice, q->st));
+        std::swap(q->psi, q->tmp);
+    } else {
+        // in place through a bounded staging ring: piece by piece, copy the outgoing
+        // piece of every peer chunk to staging, then send it and receive in place
+        u64 piece = std::min<u64>(chunk, 1ull << 26);  // 1 GiB per peer
+        int rc = scratch(q, (size_t)(G - 1) * piece * sizeof(double2));
+        if (rc) return rc;
+        double2 *stg = (double2 *)q->d_scratch;
+        for (u64 off = 0; off < chunk; off += piece) {
+            int slot = 0;
+            for (int c = 0; c < G; ++c) {
+                if (c == q->rank) continue;
+                CK(cudaMemcpyAsync(stg + (size_t)slot * piece, q->psi + c * chunk + off, piece * sizeof(double2),
+                                   cudaMemcpyDeviceToDevice, q->st));
+                ++slot;
+            }
+            NK(ncclGroupStart());
+            slot = 0;
+            for (int c = 0; c < G; ++c) {
+                if (c == q->rank) continue;
+                NK(ncclSend(stg + (size_t)slot * piece, piece * 2, ncclDouble, c, q->comm, q->st));
+                NK(ncclRecv(q->psi + c * chunk + off, piece * 2, ncclDouble, c, q->comm, q->st));
+                ++slot;
+            }
+            NK(ncclGroupEnd());
+        }
+    }
+    q->parity ^= 1;
+    return QSIM_OK;
+}
+
+int prof_events(qsim *q, cudaEvent_t *a, cudaEvent_t *b) {
+    while (q->ev_pool.size() < q->ev_used + 2) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        q->ev_pool.push_back(e);
+    }
+    *a = q->ev_pool[q->ev_used];
+    *b = q->ev_pool[q->ev_used + 1];
+    q->ev_used += 2;
+    return QSIM_OK;
+}
+
+int upload_frames(qsim *q) {
+    const int n = q->n;
+    for (int par = 0; par < (q->g ? 2 : 1); ++par) {
+        std::vector<double> hp(n), Jp((size_t)n * n, 0.0);
+        for (int a = 0; a < n; ++a) {
+            int pa = phys_pos(n, q->m, q->g, par, a);
+            hp[pa] = q->h[a];
+            for (int b = 0; b < n; ++b) Jp[(size_t)pa * n + phys_pos(n, q->m, q->g, par, b)] = q->J[(size_t)a * n + b];
+        }
+        CK(cudaMemcpyAsync(q->d_hp[par], hp.data(), sizeof(double) * n, cudaMemcpyHostToDevice, q->st));
+        CK(cudaMemcpyAsync(q->d_Jp[par], Jp.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, q->st));
+    }
+    CK(cudaStreamSynchronize(q->st));
+    return QSIM_OK;
+}
+
+int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
+    if (q->m <= qk::KT) {  // whole state in one CTA (single GPU only)
+        if ((size_t)2 * p > q->ang_cap) {
+            if (q->d_ang) cudaFree(q->d_ang);
+            q->d_ang = nullptr;
+            CK(cudaMalloc(&q->d_ang, sizeof(double) * 2 * p));
+            q->ang_cap = 2 * p;
+        }
+        std::vector<double> ang(2 * p);
+        std::copy(gam, gam + p, ang.begin());
+        std::copy(bet, bet + p, ang.begin() + p);
+        CK(cudaMemcpyAsync(q->d_ang, ang.data(), sizeof(double) * 2 * p, cudaMemcpyHostToDevice, q->st));
+        qk::SmallParams S{};
+        S.psi = q->psi;
+        S.hp = q->d_hp[0];
+        S.Jp = q->d_Jp[0];
+        S.ang = q->d_ang;
+        S.n = q->n;
+        S.p = p;
+        S.init = q->pending_plus ? 1 : 0;
+        S.reduce = 1;
+        S.a0 = std::pow(2.0, -0.5 * q->n);
+        S.res = q->d_res;
+        CK(qk::launch_small(S, q->st));
+        q->launches++;
+        // the host copy of the angles must outlive the async copy
+        CK(cudaStreamSynchronize(q->st));
+        q->pending_plus = false;
+        q->res_valid = true;
+        return QSIM_OK;
+    }
+    std::vector<PassOp> ops = build_schedule((int)q->sets.size(), q->g, p, gam, bet, q->pending_plus);
+    int last_grid = 0;
+    for (const PassOp &op : ops) {
+        const TileSet &S = q->sets[op.set];
+        qk::PassParams P = base_params(q, S);
+        std::complex<double> k1(1.0, 0.0), k2(1.0, 0.0);
+        const unsigned m1 = op.mix1 & S.own, m2 = op.mix2 & S.own;
+        P.c1 = mix_coef(op.b1, k1);
+        P.c2 = mix_coef(op.b2, k2);
+        P.mix1 = m1;
+        P.mix2 = op.phase ? m2 : 0u;
+        std::complex<double> sc = cpow_int(k1, __builtin_popcount(P.mix1)) * cpow_int(k2, __builtin_popcount(P.mix2));
+        P.scale = make_double2(sc.real(), sc.imag());
+        P.init = op.init;
+        P.phase = op.phase;
+        P.reduce = op.reduce;
+        P.gamma = op.gamma;
+        int grid = grid_for(q, S.ntiles);
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (q->prof) {
+            int rc = prof_events(q, &e0, &e1);
+            if (rc) return rc;
+            CK(cudaEventRecord(e0, q->st));
+        }
+        CK(qk::launch_pass(P, grid, q->st));
+        q->launches++;
+        if (q->prof) {
+            CK(cudaEventRecord(e1, q->st));
+            // algorithmic HBM bytes: read + write of the shard, write only for the init pass
+            q->prof_bytes.push_back((op.init ? 16.0 : 32.0) * (double)(1ull << q->m));
+        }
+        last_grid = grid;
+        if (op.swap_after) {
+            int rc = do_swap(q);
+            if (rc) return rc;
+        }
+    }
+    q->pending_plus = false;
+    return finish_reduce(q, last_grid);
+}
+
+int check_angles(const double *a, int p) {
+    for (int i = 0; i < p; ++i)
+        if (!std::isfinite(a[i])) return QSIM_EINVAL;
+    return QSIM_OK;
+}
+
+int run_reduce(qsim *q) {
+    int rc = materialize_plus(q);
+    if (rc) return rc;
+    if (q->res_valid) return QSIM_OK;
+    if (q->m <= qk::KT) {
+        qk::SmallParams S{};
+        S.psi = q->psi;
+        S.hp = q->d_hp[0];
+        S.Jp = q->d_Jp[0];
+        S.ang = nullptr;
+        S.n = q->n;
+        S.p = 0;
+        S.init = 0;
+        S.reduce = 1;
+        S.res = q->d_res;
+        CK(qk::launch_small(S, q->st));
+        q->launches++;
+        q->res_valid = true;
+        return QSIM_OK;
+    }
+    const TileSet &S = q->sets[0];
+    qk::PassParams P = base_params(q, S);
+    int grid = grid_for(q, S.ntiles);
+    CK(qk::launch_reduce(P, grid, q->st));
+    q->launches++;
+    return finish_reduce(q, grid);
+}
+
+qk::GatherParams gather_params(const qsim *q, u64 first, u64 count, const u64 *list) {
+    qk::GatherParams G{};
+    G.n = q->n;
+    G.m = q->m;
+    G.rank = (u64)q->rank;
+    G.first = first;
+    G.count = count;
+    G.list = list;
+    for (int b = 0; b < q->n; ++b) G.pos[b] = (unsigned char)phys_pos(q->n, q->m, q->g, q->parity, b);
+    return G;
+}
+
+// gather logical amplitudes (explicit list or range) into host memory; collective
+int gather_host(qsim *q, u64 first, u64 count, const uint64_t *hlist, double *out) {
+    int rc = materialize_plus(q);
+    if (rc) return rc;
+    const u64 CH = 1ull << 22;  // 64 MiB of amplitudes per round
+    for (u64 done = 0; done < count; done += CH) {
+        u64 c = std::min(CH, count - done);
+        size_t need = c * sizeof(double2) + (hlist ? c * sizeof(u64) : 0);
+        rc = scratch(q, need);
+        if (rc) return rc;
+        double2 *dout = (double2 *)q->d_scratch;
+        u64 *dlist = nullptr;
+        if (hlist) {
+            dlist = (u64 *)((char *)q->d_scratch + c * sizeof(double2));
+            CK(cudaMemcpyAsync(dlist, hlist + done, c * sizeof(u64), cudaMemcpyHostToDevice, q->st));
+        }
+        qk::GatherParams G = gather_params(q, first + done, c, dlist);
+        CK(qk::launch_gather(G, q->psi, dout, (int)std::min<u64>((c + 255) / 256, 4096), q->st));
+        q->launches++;
+        if (q->world > 1) NK(ncclAllReduce(dout, dout, c * 2, ncclDouble, ncclSum, q->comm, q->st));
+        CK(cudaMemcpyAsync(out + 2 * done, dout, c * sizeof(double2), cudaMemcpyDeviceToHost, q->st));
+        CK(cudaStreamSynchronize(q->st));
+    }
+    return QSIM_OK;
+}
+
+int create_common(qsim *q, int n, int precision, int rank, int world, const void *uid, void *buf,
+                  size_t buf_bytes, void *stream) {
+    if (precision != QSIM_FP64) return fail(q, QSIM_EUNSUPPORTED, "only QSIM_FP64 is supported");
+    if (n < 1 || n > qk::NMAX) return fail(q, QSIM_EINVAL, "n out of range [1, 40]");
+    int g = ilog2(world);
+    if (world < 1 || world > 8 || g < 0) return fail(q, QSIM_EINVAL, "world must be 1, 2, 4 or 8");
+    if (rank < 0 || rank >= world) return fail(q, QSIM_EINVAL, "rank out of range");
+    q->n = n;
+    q->g = g;
+    q->m = n - g;
+    q->rank = rank;
+    q->world = world;
+    if (world > 1 && q->m < qk::KT + 3) return fail(q, QSIM_EUNSUPPORTED, "multi-GPU needs n - log2(world) >= 15");
+    CK(cudaGetDevice(&q->dev));
+    CK(cudaDeviceGetAttribute(&q->num_sms, cudaDevAttrMultiProcessorCount, q->dev));
+    CK(qk::setup_kernels());
+    if (stream) {
+        q->st = (cudaStream_t)stream;
+    } else {
+        CK(cudaStreamCreateWithFlags(&q->st, cudaStreamNonBlocking));
+        q->own_stream = true;
+    }
+    const size_t bytes = (size_t)16 << q->m;
+    if (buf) {
+        if (buf_bytes < bytes) return fail(q, QSIM_EINVAL, "state_buf too small");
+        q->psi = (double2 *)buf;
+        q->user_buf = buf;
+    } else {
+        cudaError_t e = cudaMalloc(&q->psi, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(q, QSIM_ENOMEM, "cannot allocate " + std::to_string(bytes) + " bytes for 2^" +
+                                            std::to_string(q->m) + " amplitudes");
+        }
+        q->own_psi = true;
+    }
+    for (int par = 0; par < 2; ++par) {
+        CK(cudaMalloc(&q->d_hp[par], sizeof(double) * n));
+        CK(cudaMalloc(&q->d_Jp[par], sizeof(double) * n * n));
+    }
+    CK(cudaMalloc(&q->d_part, sizeof(double) * 2 * 4 * q->num_sms));
+    CK(cudaMalloc(&q->d_res, sizeof(double) * 2));
+    if (q->m > qk::KT) q->sets = build_sets(q->m);
+    if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, uid, sizeof(id));
+        NK(ncclCommInitRank(&q->comm, world, id, rank));
+        // out-of-place swap buffer when it leaves >= 8 GiB free, else in-place staging
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        if (fr > bytes + (8ull << 30)) {
+            if (cudaMalloc(&q->tmp, bytes) != cudaSuccess) {
+                cudaGetLastError();
+                q->tmp = nullptr;
+            }
+        }
+    }
+    q->pending_plus = true;
+    return QSIM_OK;
+}
+
+}  // namespace
+
+// =========================================================================== C-ABI
+extern "C" {
+
+int qsim_create(int n, int precision, qsim_t **out) {
+    return qsim_create_ex(n, precision, 0, 1, nullptr, nullptr, 0, nullptr, out);
+}
+
+int qsim_create_ex(int n, int precision, int rank, int world, const void *nccl_unique_id, void *state_buf,
+                   size_t buf_bytes, void *cuda_stream, qsim_t **out) {
+    if (!out) return fail(nullptr, QSIM_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (world > 1 && !nccl_unique_id) return fail(nullptr, QSIM_EINVAL, "nccl_unique_id is NULL");
+    qsim *q = new qsim();
+    int rc = create_common(q, n, precision, rank, world, nccl_unique_id, state_buf, buf_bytes, cuda_stream);
+    if (rc != QSIM_OK) {
+        g_create_error = q->err;
+        qsim_destroy(q);
+        return rc;
+    }
+    *out = q;
+    return QSIM_OK;
+}
+
+int qsim_destroy(qsim_t *q) {
+    if (!q) return QSIM_EINVAL;
+    if (q->st) cudaStreamSynchronize(q->st);
+    if (q->comm) ncclCommDestroy(q->comm);
+    if (q->psi && q->psi != q->user_buf) cudaFree(q->psi);
+    if (q->tmp && q->tmp != q->user_buf) cudaFree(q->tmp);
+    for (int par = 0; par < 2; ++par) {
+        if (q->d_hp[par]) cudaFree(q->d_hp[par]);
+        if (q->d_Jp[par]) cudaFree(q->d_Jp[par]);
+    }
+    if (q->d_part) cudaFree(q->d_part);
+    if (q->d_res) cudaFree(q->d_res);
+    if (q->d_ang) cudaFree(q->d_ang);
+    if (q->d_scratch) cudaFree(q->d_scratch);
+    for (cudaEvent_t e : q->ev_pool) cudaEventDestroy(e);
+    if (q->own_stream && q->st) cudaStreamDestroy(q->st);
+    delete q;
+    return QSIM_OK;
+}
+
+int qsim_set_ising(qsim_t *q, const double *h, const double *J) {
+    if (!q) return QSIM_EINVAL;
+    if (!h || !J) return fail(q, QSIM_EINVAL, "h or J is NULL");
+    const int n = q->n;
+    std::vector<double> hh(h, h + n), JJ((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i) {
+        if (!std::isfinite(hh[i])) return fail(q, QSIM_EINVAL, "h contains NaN/Inf");
+        for (int j = i + 1; j < n; ++j) {
+            double v = J[(size_t)i * n + j];
+            if (!std::isfinite(v)) return fail(q, QSIM_EINVAL, "J contains NaN/Inf");
+            JJ[(size_t)i * n + j] = v;
+            JJ[(size_t)j * n + i] = v;
+        }
+    }
+    q->h = hh;
+    q->J = JJ;
+    int rc = upload_frames(q);
+    if (rc) return rc;
+    q->has_ising = true;
+    q->res_valid = false;
+    return QSIM_OK;
+}
+
+int qsim_init_plus(qsim_t *q) {
+    if (!q) return QSIM_EINVAL;
+    q->pending_plus = true;
+    q->res_valid = false;
+    return QSIM_OK;
+}
+
+int qsim_apply_qaoa(qsim_t *q, const double *gamma, const double *beta, int p) {
+    if (!q) return QSIM_EINVAL;
+    if (!gamma || !beta || p < 1) return fail(q, QSIM_EINVAL, "need gamma, beta and p >= 1");
+    if (check_angles(gamma, p) || check_angles(beta, p)) return fail(q, QSIM_EINVAL, "angles contain NaN/Inf");
+    if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
+    q->res_valid = false;
+    return apply_layers(q, gamma, beta, p);
+}
+
+int qsim_aqa_angles(double T, int p, const double *s, const double *A, const double *B, int n_knots,
+                    double *gamma_out, double *beta_out) {
+    if (p < 2 || n_knots < 2 || !s || !A || !B || !gamma_out || !beta_out) return QSIM_EINVAL;
+    if (!std::isfinite(T)) return QSIM_EINVAL;
+    for (int j = 0; j < n_knots; ++j) {
+        if (!std::isfinite(s[j]) || !std::isfinite(A[j]) || !std::isfinite(B[j])) return QSIM_EINVAL;
+        if (j > 0 && !(s[j] > s[j - 1])) return QSIM_EINVAL;
+    }
+    if (s[0] != 0.0 || s[n_knots - 1] != 1.0) return QSIM_EINVAL;
+    const double tau = T / p;  // t_anneal = (n_steps + 1) tau = p tau = T
+    for (int k = 1; k <= p; ++k) {
+        const double sk = (double)(k - 1) / (double)(p - 1);  // s_k = (k-1)/(p-1)
+        gamma_out[k - 1] = tau * pwl(s, B, n_knots, sk);    // eq:gamma_k
+        if (k < p) {
+            const double sk1 = (double)k / (double)(p - 1);
+            beta_out[k - 1] = -tau * (pwl(s, A, n_knots, sk1) + pwl(s, A, n_knots, sk)) / 2.0;  // eq:beta_k
+        } else {
+            beta_out[k - 1] = -tau * pwl(s, A, n_knots, sk) / 2.0;  // beta_p
+        }
+    }
+    return QSIM_OK;
+}
+
+int qsim_apply_aqa(qsim_t *q, double T, int p, const double *s, const double *A, const double *B, int n_knots) {
+    if (!q) return QSIM_EINVAL;
+    if (p < 2) return fail(q, QSIM_EINVAL, "AQA needs p >= 2 (s_k = (k-1)/(p-1))");
+    std::vector<double> g(p), b(p);
+    if (qsim_aqa_angles(T, p, s, A, B, n_knots, g.data(), b.data()) != QSIM_OK)
+        return fail(q, QSIM_EINVAL, "invalid schedule (knots must rise strictly from s=0 to s=1)");
+    return qsim_apply_qaoa(q, g.data(), b.data(), p);
+}
+
+int qsim_expect_hc(qsim_t *q, double *out) {
+    if (!q) return QSIM_EINVAL;
+    if (!out) return fail(q, QSIM_EINVAL, "out is NULL");
+    if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
+    int rc = run_reduce(q);
+    if (rc) return rc;
+    double r[2];
+    CK(cudaMemcpyAsync(r, q->d_res, sizeof(r), cudaMemcpyDeviceToHost, q->st));
+    CK(cudaStreamSynchronize(q->st));
+    *out = r[0];
+    return QSIM_OK;
+}
+
+int qsim_norm2(qsim_t *q, double *out) {
+    if (!q) return QSIM_EINVAL;
+    if (!out) return fail(q, QSIM_EINVAL, "out is NULL");
+    if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
+    int rc = run_reduce(q);
+    if (rc) return rc;
+    double r[2];
+    CK(cudaMemcpyAsync(r, q->d_res, sizeof(r), cudaMemcpyDeviceToHost, q->st));
+    CK(cudaStreamSynchronize(q->st));
+    *out = r[1];
+    return QSIM_OK;
+}
+
+int qsim_success_prob(qsim_t *q, const uint64_t *gs, int count, double *out) {
+    if (!q) return QSIM_EINVAL;
+    if (!gs || count < 1 || !out) return fail(q, QSIM_EINVAL, "need ground_states, count >= 1, out");
+    for (int i = 0; i < count; ++i)
+        if (gs[i] >> q->n) return fail(q, QSIM_ERANGE, "ground state label >= 2^n");
+    std::vector<double> amp(2 * (size_t)count);
+    int rc = gather_host(q, 0, (u64)count, gs, amp.data());
+    if (rc) return rc;
+    double acc = 0.0;
+    for (int i = 0; i < count; ++i) acc += amp[2 * i] * amp[2 * i] + amp[2 * i + 1] * amp[2 * i + 1];
+    *out = acc;
+    return QSIM_OK;
+}
+
+int qsim_get_amplitudes(qsim_t *q, uint64_t first, uint64_t count, double *out) {
+    if (!q) return QSIM_EINVAL;
+    if (!out && count) return fail(q, QSIM_EINVAL, "out is NULL");
+    if (count == 0) return QSIM_OK;
+    if (first >> q->n || count > (1ull << q->n) - first) return fail(q, QSIM_ERANGE, "range exceeds 2^n");
+    return gather_host(q, first, count, nullptr, out);
+}
+
+int qsim_energies(qsim_t *q, uint64_t first, uint64_t count, double *out) {
+    if (!q) return QSIM_EINVAL;
+    if (!out && count) return fail(q, QSIM_EINVAL, "out is NULL");
+    if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
+    if (count == 0) return QSIM_OK;
+    if (first >> q->n || count > (1ull << q->n) - first) return fail(q, QSIM_ERANGE, "range exceeds 2^n");
+    qk::ProbeSet PS{};
+    PS.k = std::min(qk::KT, q->m);
+    PS.lmask = 0;
+    for (int i = 0; i < PS.k; ++i) {
+        PS.L[i] = q->m > qk::KT ? q->sets[0].L[i] : i;
+        PS.lmask |= 1ull << PS.L[i];
+    }
+    const u64 CH = 1ull << 23;
+    for (u64 done = 0; done < count; done += CH) {
+        u64 c = std::min(CH, count - done);
+        int rc = scratch(q, c * sizeof(double));
+        if (rc) return rc;
+        qk::GatherParams G = gather_params(q, first + done, c, nullptr);
+        CK(qk::launch_energy_probe(G, q->d_hp[q->parity], q->d_Jp[q->parity], PS, (double *)q->d_scratch,
+                                   (int)std::min<u64>((c + 255) / 256, 4096), q->st));
+        q->launches++;
+        CK(cudaMemcpyAsync(out + done, q->d_scratch, c * sizeof(double), cudaMemcpyDeviceToHost, q->st));
+        CK(cudaStreamSynchronize(q->st));
+    }
+    return QSIM_OK;
+}
+
+int qsim_sync(qsim_t *q) {
+    if (!q) return QSIM_EINVAL;
+    CK(cudaStreamSynchronize(q->st));
+    return QSIM_OK;
+}
+
+int qsim_plan_counts(int n, int world, int p, int *passes_out, int *swaps_out, uint64_t *amps_sent_out) {
+    int g = ilog2(world);
+    if (n < 1 || n > qk::NMAX || world < 1 || world > 8 || g < 0 || p < 1) return QSIM_EINVAL;
+    int m = n - g;
+    if (world > 1 && m < qk::KT + 3) return QSIM_EINVAL;
+    int passes = 0, swaps = 0;
+    if (m <= qk::KT) {
+        passes = 1;
+    } else {
+        std::vector<double> z(p, 0.0);
+        auto ops = build_schedule((int)build_sets(m).size(), g, p, z.data(), z.data(), true);
+        passes = (int)ops.size();
+        for (auto &o : ops) swaps += o.swap_after ? 1 : 0;
+    }
+    if (passes_out) *passes_out = passes;
+    if (swaps_out) *swaps_out = swaps;
+    if (amps_sent_out) *amps_sent_out = g ? (uint64_t)(world - 1) << (m - g) : 0;
+    return QSIM_OK;
+}
+
+int qsim_plan_positions(int n, int world, int layers, int *pos_out) {
+    int g = ilog2(world);
+    if (n < 1 || n > qk::NMAX || g < 0 || world > 8 || layers < 0 || !pos_out) return QSIM_EINVAL;
+    int m = n - g;
+    for (int qb = 0; qb < n; ++qb) pos_out[qb] = phys_pos(n, m, g, layers & 1, qb);
+    return QSIM_OK;
+}
+
+int qsim_profile_enable(qsim_t *q, int on) {
+    if (!q) return QSIM_EINVAL;
+    q->prof = on != 0;
+    q->ev_used = 0;
+    q->prof_bytes.clear();
+    return QSIM_OK;
+}
+
+int qsim_profile_read(qsim_t *q, double *ms_sum, uint64_t *count, double *bytes_sum) {
+    if (!q || !ms_sum || !count || !bytes_sum) return QSIM_EINVAL;
+    CK(cudaStreamSynchronize(q->st));
+    double ms = 0.0, by = 0.0;
+    size_t npass = q->ev_used / 2;
+    for (size_t i = 0; i < npass; ++i) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, q->ev_pool[2 * i], q->ev_pool[2 * i + 1]));
+        ms += t;
+        by += q->prof_bytes[i];
+    }
+    *ms_sum = ms;
+    *count = npass;
+    *bytes_sum = by;
+    q->ev_used = 0;
+    q->prof_bytes.clear();
+    return QSIM_OK;
+}
+
+uint64_t qsim_kernel_launches(const qsim_t *q) { return q ? q->launches : 0; }
+
+const char *qsim_last_error(const qsim_t *q) { return q ? q->err.c_str() : g_create_error.c_str(); }
+
+const char *qsim_version(void) { return "qsim-b200 0.1 (sm_100a, FP64)"; }
+
+int qsim_nccl_unique_id(void *out128) {
+    if (!out128) return QSIM_EINVAL;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return QSIM_ENCCL;
+    std::memcpy(out128, &id, sizeof(id));
+    return QSIM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,144 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol include/qsim.h
+declares, and its host-only logic (AQA angles, pass planner, permutation bookkeeping)
+is right.  No compute calls need a GPU here."""
+import ctypes
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tests.conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "qsim.h")
+
+
+@pytest.fixture(scope="module")
+def Q():
+    from paper_2104_03293_b200 import build
+
+    build.build()
+    from paper_2104_03293_b200 import qsim
+
+    return qsim
+
+
+def header_symbols():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(qsim_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_header_symbols_exported(Q):
+    syms = header_symbols()
+    assert len(syms) >= 18
+    lib = ctypes.CDLL(Q.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert sorted(Q.EXPORTS) == syms
+
+
+def test_library_is_sm100a(Q):
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", Q.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version(Q):
+    assert "sm_100a" in Q.qsim_version()
+
+
+def test_aqa_angles_golden(Q, golden_dir):
+    g = json.load(open(os.path.join(golden_dir, "aqa_angles_toy.json")))
+    sch = g["schedule"]
+    for case in g["cases"]:
+        gam, bet = Q.qsim_aqa_angles(case["T"], case["p"], sch["s"], sch["A"], sch["B"])
+        assert list(bet) == case["beta"] and list(gam) == case["gamma"]
+
+
+def test_aqa_angles_match_oracle(Q):
+    from oracle import oracle as o
+    from paper_2104_03293_b200 import instances as inst
+
+    s, A, B = inst.dw_like_schedule()
+    for p in (2, 5, 16, 51):
+        T = 0.4 * p
+        g1, b1 = Q.qsim_aqa_angles(T, p, s, 2 * np.pi * A, 2 * np.pi * B)
+        g2, b2 = o.aqa_angles(T, p, s, 2 * np.pi * A, 2 * np.pi * B)
+        assert np.max(np.abs(g1 - g2)) <= 1e-15 * max(1, np.max(np.abs(g2)))
+        assert np.max(np.abs(b1 - b2)) <= 1e-15 * max(1, np.max(np.abs(b2)))
+
+
+def test_aqa_angles_errors(Q):
+    with pytest.raises(Q.QsimError):
+        Q.qsim_aqa_angles(1.0, 1, [0, 1], [1, 0], [0, 1])  # p < 2 (reading R8)
+    with pytest.raises(Q.QsimError):
+        Q.qsim_aqa_angles(1.0, 3, [0, 0.5, 0.4, 1], [1, 1, 1, 0], [0, 0, 0, 1])  # non-monotone knots
+    with pytest.raises(Q.QsimError):
+        Q.qsim_aqa_angles(float("nan"), 3, [0, 1], [1, 0], [0, 1])
+
+
+@pytest.mark.parametrize("n", [13, 20, 24, 30, 33])
+def test_plan_single_gpu_boustrophedon(Q, n):
+    # sets: 12 bits, then runs of <= 9 -> P sets; (P-1) p + 1 passes
+    P = 1 + -(-(n - 12) // 9)
+    for p in (1, 2, 7):
+        passes, swaps, amps = Q.qsim_plan_counts(n, 1, p)
+        assert passes == (P - 1) * p + 1 and swaps == 0 and amps == 0
+
+
+def test_plan_small_state_single_launch(Q):
+    assert Q.qsim_plan_counts(12, 1, 5)[0] == 1
+
+
+@pytest.mark.parametrize("n,world", [(18, 2), (33, 2), (33, 4), (33, 8), (36, 8)])
+def test_plan_multi_gpu_transfer_law(Q, n, world):
+    """One swap per layer; each rank sends (G-1)/G of its shard per swap (SURVEY §4 ledger law)."""
+    g = world.bit_length() - 1
+    m = n - g
+    P = 1 + -(-(m - 12) // 9)
+    for p in (1, 3):
+        passes, swaps, amps = Q.qsim_plan_counts(n, world, p)
+        assert swaps == p
+        assert passes == P * p + 1
+        assert amps * world == (world - 1) * (1 << m)
+
+
+def test_plan_rejects_bad_layouts(Q):
+    with pytest.raises(Q.QsimError):
+        Q.qsim_plan_counts(33, 3, 1)
+    with pytest.raises(Q.QsimError):
+        Q.qsim_plan_counts(14, 8, 1)  # n - g < 15
+
+
+def test_plan_positions_swap_involution(Q):
+    n, world = 20, 4
+    p0 = Q.qsim_plan_positions(n, world, 0)
+    p1 = Q.qsim_plan_positions(n, world, 1)
+    p2 = Q.qsim_plan_positions(n, world, 2)
+    assert p0 == list(range(n)) and p2 == p0
+    assert sorted(p1) == list(range(n))
+    # top 2 local qubits <-> 2 global qubits
+    assert p1[16:18] == [18, 19] and p1[18:20] == [16, 17] and p1[:16] == list(range(16))
+
+
+def test_create_without_gpu_fails_loudly(Q):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(Q.QsimError) as ei:
+        Q.qsim_create(10)
+    assert ei.value.code == Q.QSIM_ECUDA
+
+
+def test_create_rejects_bad_arguments(Q):
+    with pytest.raises(Q.QsimError) as ei:
+        Q.qsim_create(10, Q.QSIM_FP32)
+    assert ei.value.code == Q.QSIM_EUNSUPPORTED
+    with pytest.raises(Q.QsimError) as ei:
+        Q.qsim_create(0)
+    assert ei.value.code == Q.QSIM_EINVAL

@@ -1,0 +1,298 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by
+element, on seeded synthetic inputs.
+
+Bars (BASELINE.json north_star; readings R12-R14):
+  * amplitudes: max |psi_gpu - psi_oracle| <= 1e-10 and ||psi_gpu - psi_oracle||_2 <= 1e-12
+  * <H_C>: |d| <= 1e-9 * max(|ref|, sum |psi|^2 |E|);  P_success, norm: relative 1e-9
+  * E(z): bit-exact (dyadic instances)
+"""
+import numpy as np
+import pytest
+
+from oracle import closed_forms as cf
+from oracle import oracle as o
+from oracle import problems as op
+from paper_2104_03293_b200 import instances as inst
+
+pytestmark = pytest.mark.gpu
+
+AMP_TOL = 1e-10
+L2_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def Q():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2104_03293_b200 import build
+
+    build.build()
+    from paper_2104_03293_b200 import qsim
+
+    return qsim
+
+
+def rand_angles(p, seed):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(-2.0, 2.0, p), rng.uniform(-np.pi, np.pi, p)
+
+
+def assert_state_close(got, ref):
+    d = got - ref
+    assert np.max(np.abs(d)) <= AMP_TOL, np.max(np.abs(d))
+    assert np.linalg.norm(d) <= L2_TOL, np.linalg.norm(d)
+
+
+def assert_expect_close(got, h, J, psi_ref):
+    ref, scale = o.expect_hc(h, J, psi_ref, with_abs=True)
+    assert abs(got - ref) <= 1e-9 * max(abs(ref), scale, 1e-300), (got, ref)
+
+
+def run_gpu(Q, h, J, gam, bet, n=None):
+    n = len(h) if n is None else n
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        s.init_plus()
+        s.apply_qaoa(gam, bet)
+        return s.amplitudes(), s.expect_hc(), s.norm2(), s.launches
+
+
+# ------------------------------------------------------------------ small states (one CTA)
+@pytest.mark.parametrize("n,p", [(1, 3), (2, 2), (5, 4), (9, 3), (12, 5)])
+def test_small_state_parity(Q, n, p):
+    h, J = inst.random_ising(n, 100 + n)
+    g, b = rand_angles(p, n)
+    psi, e, nrm, _ = run_gpu(Q, h, J, g, b)
+    ref = o.qaoa_state(h, J, g, b)
+    assert_state_close(psi, ref)
+    assert_expect_close(e, h, J, ref)
+    assert abs(nrm - 1.0) <= 1e-12
+
+
+# ------------------------------------------------------------------ tiled passes (m >= 13)
+@pytest.mark.parametrize("n,p", [(13, 1), (13, 3), (14, 2), (16, 4), (20, 3), (21, 2), (22, 5), (24, 2)])
+def test_tiled_parity(Q, n, p):
+    h, J = inst.random_ising(n, 200 + n)
+    g, b = rand_angles(p, 300 + n + p)
+    psi, e, nrm, launches = run_gpu(Q, h, J, g, b)
+    ref = o.qaoa_state(h, J, g, b)
+    assert_state_close(psi, ref)
+    assert_expect_close(e, h, J, ref)
+    assert abs(nrm - 1.0) <= 1e-12
+    assert launches > 0
+
+
+def test_mixer_forms_and_edge_angles(Q):
+    """beta where |tan beta| > 1 (form 1), exactly pi/4 and pi/2, beta = 0, gamma = 0."""
+    n = 15
+    h, J = inst.random_ising(n, 7)
+    for bet in ([np.pi / 2, 0.0, np.pi / 4], [1.3, -1.3, 2.9], [0.0, 0.0, 0.0], [np.pi / 4, -np.pi / 4, 3 * np.pi / 4]):
+        gam = [0.3, 0.0, -1.1]
+        psi, e, _, _ = run_gpu(Q, h, J, gam, bet)
+        ref = o.qaoa_state(h, J, gam, bet)
+        assert_state_close(psi, ref)
+
+
+def test_trivial_problem_P7(Q):
+    n = 17
+    g, b = rand_angles(4, 3)
+    psi, e, _, _ = run_gpu(Q, np.zeros(n), np.zeros((n, n)), g, b)
+    ref = np.exp(-1j * n * np.sum(b)) * 2.0 ** (-n / 2)
+    assert np.max(np.abs(psi - ref)) <= AMP_TOL
+    assert abs(e) <= 1e-12
+
+
+def test_continue_without_init(Q):
+    """apply(g1,b1) then apply(g2,b2) == apply(g1+g2, b1+b2) (second call loads the state)."""
+    n = 18
+    h, J = inst.random_ising(n, 9)
+    g, b = rand_angles(5, 9)
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        s.init_plus()
+        s.apply_qaoa(g[:2], b[:2])
+        s.apply_qaoa(g[2:], b[2:])
+        psi = s.amplitudes()
+        e = s.expect_hc()
+    ref = o.qaoa_state(h, J, g, b)
+    assert_state_close(psi, ref)
+    assert_expect_close(e, h, J, ref)
+
+
+def test_reinit_and_plus_state(Q):
+    n = 16
+    h, J = inst.random_ising(n, 10)
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        s.apply_qaoa([0.4], [0.2])
+        s.init_plus()
+        psi = s.amplitudes()
+        assert np.all(psi == 2.0 ** (-n / 2))
+        assert abs(s.expect_hc()) <= 1e-12
+        assert abs(s.norm2() - 1.0) <= 1e-13
+
+
+def test_aqa_parity(Q):
+    n = 20
+    a, x_star = inst.exact_cover(n, F=60, seed=1, planted_rows=5, weight=9)
+    h, J, C = op.exact_cover_to_ising(a)
+    r = op.rescale_factor(h, J)
+    s, A, B = inst.dw_like_schedule()
+    A = 2 * np.pi * A
+    B = 2 * np.pi * B / r
+    p, T = 8, 0.4 * 8
+    with Q.QSim(n) as sim:
+        sim.set_ising(h, J)
+        sim.init_plus()
+        sim.apply_aqa(T, p, s, A, B)
+        psi = sim.amplitudes()
+        e = sim.expect_hc()
+        z_star = int(sum(int(x_star[i]) << i for i in range(n)))
+        ps = sim.success_prob([z_star])
+    ref = o.aqa_state(h, J, T, p, s, A, B)
+    assert_state_close(psi, ref)
+    assert_expect_close(e, h, J, ref)
+    pref = o.success_prob(ref, [z_star])
+    assert abs(ps - pref) <= 1e-9 * pref
+
+
+def test_energies_bit_exact(Q):
+    for n, seed in [(6, 1), (12, 2), (13, 3), (20, 4), (22, 5)]:
+        h, J = inst.random_ising(n, seed)
+        with Q.QSim(n) as s:
+            s.set_ising(h, J)
+            e = s.energies()
+        assert np.array_equal(e, o.energies(h, J))
+
+
+def test_two_sat_config1_grid(Q):
+    """configs[0]: n=12 planted 2-SAT, AQA p=5 and the p=1 64x64 grid."""
+    n = 12
+    clauses, x_star = inst.planted_2sat(n, seed=0)
+    h, J, C = op.two_sat_to_ising(n, clauses)
+    gs, emin, cnt = o.ground_states(h, J)
+    assert cnt == 1
+    s_, A, B = inst.toy_schedule()
+    with Q.QSim(n) as sim:
+        sim.set_ising(h, J)
+        sim.init_plus()
+        sim.apply_aqa(2.5, 5, s_, A, B)
+        ref = o.aqa_state(h, J, 2.5, 5, s_, A, B)
+        assert_state_close(sim.amplitudes(), ref)
+        assert abs(sim.success_prob(gs) - o.success_prob(ref, gs)) <= 1e-9 * o.success_prob(ref, gs)
+        betas = np.arange(64) * np.pi / 64
+        gammas = np.arange(64) * 2 * np.pi / 64
+        worst = 0.0
+        for bi in range(0, 64, 3):
+            for gi in range(0, 64, 3):
+                sim.init_plus()
+                sim.apply_qaoa([gammas[gi]], [betas[bi]])
+                e = sim.expect_hc()
+                ref = o.qaoa_state(h, J, [gammas[gi]], [betas[bi]])
+                er, sc = o.expect_hc(h, J, ref, with_abs=True)
+                worst = max(worst, abs(e - er) / max(abs(er), sc))
+        assert worst <= 1e-9
+
+
+# ------------------------------------------------------------------ errors
+def test_error_codes(Q):
+    with pytest.raises(Q.QsimError) as ei:
+        Q.qsim_create(12, Q.QSIM_FP32)
+    assert ei.value.code == Q.QSIM_EUNSUPPORTED
+    with Q.QSim(14) as s:
+        with pytest.raises(Q.QsimError) as ei:
+            s.apply_qaoa([0.1], [0.2])
+        assert ei.value.code == Q.QSIM_ESTATE
+        h, J = inst.random_ising(14, 1)
+        with pytest.raises(Q.QsimError) as ei:
+            s.set_ising(np.full(14, np.nan), J)
+        assert ei.value.code == Q.QSIM_EINVAL
+        s.set_ising(h, J)
+        with pytest.raises(Q.QsimError) as ei:
+            s.apply_qaoa([], [])
+        assert ei.value.code == Q.QSIM_EINVAL
+        with pytest.raises(Q.QsimError) as ei:
+            s.apply_qaoa([np.inf], [0.1])
+        assert ei.value.code == Q.QSIM_EINVAL
+        with pytest.raises(Q.QsimError) as ei:
+            Q.qsim_get_amplitudes(s.h, (1 << 14) - 1, 2)
+        assert ei.value.code == Q.QSIM_ERANGE
+        with pytest.raises(Q.QsimError) as ei:
+            s.success_prob([1 << 14])
+        assert ei.value.code == Q.QSIM_ERANGE
+        with pytest.raises(Q.QsimError) as ei:
+            s.apply_aqa(1.0, 1, [0, 1], [1, 0], [0, 1])
+        assert ei.value.code == Q.QSIM_EINVAL
+
+
+# ------------------------------------------------------------------ full size (bench config)
+@pytest.fixture(scope="module")
+def big30(Q):
+    """The bench launch configuration (n=30, one GPU): one handle reused by the tests."""
+    s = Q.QSim(30)
+    yield s
+    s.close()
+
+
+def test_full_size_p1_closed_form_expectation(Q, big30):
+    n = 30
+    h, J = inst.random_ising(n, 31)
+    big30.set_ising(h, J)
+    for g, b in [(0.23, 0.41), (1.1, -0.7)]:
+        big30.init_plus()
+        big30.apply_qaoa([g], [b])
+        e = big30.expect_hc()
+        ref = cf.p1_expect_hc(h, J, g, b)
+        scale = np.sum(np.abs(h)) + np.sum(np.abs(np.triu(J, 1)))
+        assert abs(e - ref) <= 1e-9 * max(abs(ref), 1.0) + 1e-12 * scale, (e, ref)
+        assert abs(big30.norm2() - 1.0) <= 1e-11
+
+
+def test_full_size_product_state(Q, big30):
+    n, p = 30, 6
+    h, J = inst.product_ising(n, 5)
+    g, b = rand_angles(p, 55)
+    big30.set_ising(h, J)
+    big30.init_plus()
+    big30.apply_qaoa(g, b)
+    zs = inst.sample_indices(n, 64, seed=3)
+    got = np.array([big30.amplitudes(int(z), 1)[0] for z in zs])
+    ref = cf.product_amplitudes(h, g, b, zs)
+    assert np.max(np.abs(got - ref)) <= AMP_TOL
+    assert np.max(np.abs(got - ref)) <= 1e-10 * np.max(np.abs(ref))
+
+
+def test_full_size_cluster_instance(Q, big30):
+    n, p = 30, 4
+    clusters = inst.spread_clusters(n, 6, seed=4)
+    h, J = inst.cluster_ising(n, clusters, seed=8)
+    g, b = rand_angles(p, 66)
+    big30.set_ising(h, J)
+    big30.init_plus()
+    big30.apply_qaoa(g, b)
+    e = big30.expect_hc()
+    comp = cf.ClusterComposition(h, J, clusters, g, b)
+    assert abs(e - comp.expect) <= 1e-9 * max(abs(comp.expect), 1.0)
+    zs = inst.sample_indices(n, 64, seed=5)
+    got = np.array([big30.amplitudes(int(z), 1)[0] for z in zs])
+    ref = comp.amplitudes(zs)
+    assert np.max(np.abs(got - ref)) <= AMP_TOL
+    # contiguous block read through the full gather path
+    blk = big30.amplitudes(12345, 4096)
+    assert np.max(np.abs(blk - comp.amplitudes(np.arange(12345, 12345 + 4096)))) <= AMP_TOL
+
+
+def test_full_size_energies_sampled(Q, big30):
+    n = 30
+    a, x_star = inst.exact_cover(n, seed=0)
+    h, J, C = op.exact_cover_to_ising(a)
+    big30.set_ising(h, J)
+    zs = inst.sample_indices(n, 20000, seed=6)
+    first = int(zs[100])
+    cnt = min(20000, (1 << n) - first)
+    e = big30.energies(first, cnt)
+    assert np.array_equal(e, o.energies(h, J, first, cnt))
+    z_star = int(sum(int(x_star[i]) << i for i in range(n)))
+    assert big30.energies(z_star, 1)[0] + C == 0.0
