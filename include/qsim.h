@@ -154,6 +154,11 @@ int qsim_nccl_unique_id(void *out128);
 int qsim_profile_enable(qsim_t *q, int on);
 int qsim_profile_read(qsim_t *q, double *ms_sum, uint64_t *count, double *bytes_sum);
 
+/* Diagnostic micro-benchmark (modifies the state): time `reps` back-to-back launches of
+ * the tile pass over tile set `set` (0 = bits 0..11, 1.. = the run sets in ascending bit
+ * order) with phase on/off, on the handle's stream; *ms_out = mean ms per launch. */
+int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out);
+
 /* Number of kernels the library has launched on this handle (for bench reporting). */
 uint64_t qsim_kernel_launches(const qsim_t *q);
 

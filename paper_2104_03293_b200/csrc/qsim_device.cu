@@ -2,160 +2,195 @@
 #include "qsim_device.h"
 #include "qsim_kernels.cuh"
 
+#include <algorithm>
+
 namespace qk {
 
 // dynamic shared memory layout of the pass / reduce kernels
 struct SmemLayout {
-    static constexpr size_t tile = SM_TILE_BYTES;                 // 64 KiB tile
-    static constexpr size_t tables = sizeof(TileTables);
-    static constexpr size_t hj = sizeof(double) * (NMAX + NMAX * NMAX);
-    static constexpr size_t total = tile + ((tables + 15) / 16) * 16 + hj;
+    static constexpr size_t tile = SM_TILE_BYTES;  // 64 KiB tile exchange buffer
+    static constexpr size_t cta = ((sizeof(CtaShared) + 15) / 16) * 16;
+    static constexpr size_t total = tile + cta;
 };
+static_assert(sizeof(TileRec) == TILE_REC_BYTES, "TileRec size");
 
-__device__ __forceinline__ void load_hj(double *sh, double *sJ, const double *hp, const double *Jp, int n) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) sh[i] = hp[i];
-    for (int i = threadIdx.x; i < n * n; i += blockDim.x) sJ[i] = Jp[i];
+// ============================================================ per-tile fields (pre-pass)
+// For every tile u of the pass's tile set: h'_i(z_H) (12 tile bits), E_H(z_H) and, for
+// phase passes, their phase factors e^{-i gamma (.)}.  One thread per tile; ~0.1% of a
+// pass's time, and it removes all per-tile serial work from the streaming kernel.
+__global__ void __launch_bounds__(128) tile_fields_kernel(const PassParams P, TileRec *rec) {
+    __shared__ double sh[NMAX];
+    __shared__ double sJ[NMAX * NMAX];
+    const int n = P.n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sh[i] = P.hp[i];
+    for (int i = threadIdx.x; i < n * n; i += blockDim.x) sJ[i] = P.Jp[i];
+    __syncthreads();
+    for (u64 u = blockIdx.x * (u64)blockDim.x + threadIdx.x; u < P.ntiles; u += (u64)gridDim.x * blockDim.x) {
+        const u64 X = (tile_base(P, u) | P.xglob) ^ P.flip;
+        TileRec r;
+        double eh = 0.0;
+        for (int j = 0; j < n; ++j)
+            if (!((P.lmask >> j) & 1ull)) eh += eh_term(sh, sJ, n, j, X, P.lmask);
+        r.e[KT] = eh;
+#pragma unroll
+        for (int i = 0; i < KT; ++i) r.e[i] = field_hprime(sh, sJ, n, P.L[i], X, P.lmask);
+        if (P.phase) {
+#pragma unroll
+            for (int i = 0; i <= KT; ++i) r.f[i] = expmi(P.gamma * r.e[i]);
+        } else {
+#pragma unroll
+            for (int i = 0; i <= KT; ++i) r.f[i] = make_double2(1.0, 0.0);
+        }
+        r.pad = 0.0;
+        rec[u] = r;
+    }
 }
 
 // ================================================================== tile pass kernel
-// One HBM sweep of the shard: [init | load] -> mix1 (A,B,C) -> [phase -> mix2 (C,B,A)]
-// -> [reduce] -> store.  Grid-stride over tiles; fixed tile->CTA assignment makes the
-// reduction deterministic.
+// One HBM sweep of the shard, program KIND (PassKind):
+//   PLAIN12:  load X, mix1 X(t7..11) -> Y(t0..4) -> Z(t5,6), [scale], [reduce], store Z
+//   PLAIN_RUN: load X, mix1 X(t7..11) -> W(t3..6), [scale], [reduce], store W
+//   TURN12:   [load X, mix1 X -> Y -> Z | init in Z], phase, mix2 Z -> Y -> X, store X
+//   TURN_RUN: [load X, mix1 X -> W | init in W], phase, mix2 W -> X, store X
+// Grid-stride over tiles with a fixed tile->CTA assignment (deterministic reduction).
+constexpr unsigned MX = 0xF80u, MY = 0x01Fu, MZ = 0x060u, MW = 0x078u;
+
+// L2 prefetch of tile `ut` (if it exists): its 512 lines of 128 B (tile bits t0..t2 are the
+// low physical bits 0..2 in every set), 4 per thread, so HBM keeps streaming while the CTA
+// computes on the current tile.
+__device__ __forceinline__ void prefetch_next(const PassParams &P, u64 ut, int tid) {
+    if (!P.prefetch || ut >= P.ntiles) return;
+    const u64 tb = tile_base(P, ut);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int l = tid + q * NTHR;
+        u64 off = tb;
+#pragma unroll
+        for (int b = 0; b < 9; ++b)
+            if ((l >> b) & 1) off |= 1ull << P.L[3 + b];
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.psi + off));
+    }
+}
+
+template <int KIND>
 __global__ void __launch_bounds__(NTHR, 2) pass_kernel(const PassParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *sm = reinterpret_cast<double2 *>(smem_raw);
-    TileTables &tt = *reinterpret_cast<TileTables *>(smem_raw + SmemLayout::tile);
-    double *sh = reinterpret_cast<double *>(smem_raw + SmemLayout::tile +
-                                            ((SmemLayout::tables + 15) / 16) * 16);
-    double *sJ = sh + NMAX;
+    CtaShared &cs = *reinterpret_cast<CtaShared *>(smem_raw + SmemLayout::tile);
+    constexpr bool RUN = (KIND == K_PLAIN_RUN || KIND == K_TURN_RUN);
+    constexpr bool TURN = (KIND == K_TURN12 || KIND == K_TURN_RUN);
+    constexpr int FE = RUN ? FW : FZ;  // frame of the phase / reduction
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = P.n;
-    const bool need_e = P.phase || P.reduce;
+    const bool need_e = TURN || P.reduce;
+    const TileRec *recs = reinterpret_cast<const TileRec *>(P.rec);
+    int ft = 0;  // tile-bit flips
+#pragma unroll
+    for (int i = 0; i < KT; ++i) ft |= (int)((P.flip >> P.L[i]) & 1ull) << i;
+    const int tE = Frame<FE>::tthr(lane, warp) ^ ft;
+    const int fr = (ft >> Frame<FE>::RB) & 0x1F;
 
-    load_hj(sh, sJ, P.hp, P.Jp, n);
-    __syncthreads();
-
-    // launch-constant energy pieces of frame C
+    // launch-constant energy pieces of the phase/reduction frame
     ThreadEnergy te;
-    double2 uTT = make_double2(1.0, 0.0);
-    double2 u[4];
+    double2 pconst = P.scale;
+    double2 u[5];
+    te.eTT = 0.0;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) u[r] = make_double2(1.0, 0.0);
+    for (int r = 0; r < 5; ++r) {
+        te.w[r] = 0.0;
+        u[r] = make_double2(1.0, 0.0);
+    }
     if (need_e) {
-        te = thread_energy<2>(sJ, n, P.L, lane, warp);
-        if (P.phase) {
-            uTT = expmi(P.gamma * te.eTT);
+        te = thread_energy<FE>(P.Jp, n, P.L, lane, warp, ft);
+        if (TURN) {
+            pconst = cmul(P.scale, expmi(P.gamma * te.eTT));
 #pragma unroll
-            for (int r = 0; r < 4; ++r) u[r] = expmi(P.gamma * te.w[r]);
+            for (int r = 0; r < 5; ++r) u[r] = expmi(P.gamma * te.w[r]);
         }
-        if (tid < 16) {
-            const double e = err_of<2>(sJ, n, P.L, tid);
-            tt.eRR[tid] = e;
-            tt.PRR[tid] = P.phase ? expmi(P.gamma * e) : make_double2(1.0, 0.0);
+        if (tid < NR) {
+            const double e = err_of<FE>(P.Jp, n, P.L, tid ^ fr);
+            cs.eRR[tid] = e;
+            cs.PRR[tid] = TURN ? expmi(P.gamma * e) : make_double2(1.0, 0.0);
         }
     }
-
-    const u64 offA = thread_offset<0>(P.L, lane, warp);
-    const u64 offC = thread_offset<2>(P.L, lane, warp);
-    const u64 sA0 = 1ull << P.L[8], sA1 = 1ull << P.L[9], sA2 = 1ull << P.L[10], sA3 = 1ull << P.L[11];
-    const u64 sC0 = 1ull << P.L[4], sC1 = 1ull << P.L[5], sC2 = 1ull << P.L[6], sC3 = 1ull << P.L[7];
+    const u64 offX = thread_offset<FX>(P.L, lane, warp);
+    const u64 offS = thread_offset<RUN ? FW : FZ>(P.L, lane, warp);
 
     double acc_e = 0.0, acc_n = 0.0;
     double2 v[NR];
 
     for (u64 ut = blockIdx.x; ut < P.ntiles; ut += gridDim.x) {
-        __syncthreads();  // previous tile done with smem tile + tables
+        __syncthreads();  // previous tile done with the smem exchange buffer / launch constants visible
         const u64 tb = tile_base(P, ut);
-        if (!P.init) {
-            const double2 *src = P.psi + tb + offA;
-#pragma unroll
-            for (int j = 0; j < NR; ++j) {
-                const u64 o = ((j & 1) ? sA0 : 0) + ((j & 2) ? sA1 : 0) + ((j & 4) ? sA2 : 0) +
-                              ((j & 8) ? sA3 : 0);
-                v[j] = __ldcs(src + o);
+        const TileRec *R = recs + ut;
+        if (!TURN || !P.init) {
+            prefetch_next(P, ut + gridDim.x, tid);
+            load_tile<FX>(v, P.psi + tb + offX, P.L);
+            mix_frame<FX>(v, P.mix1 & MX, P.c1.t);
+            if (RUN) {
+                xch<FX, FW>(v, sm, lane, warp);
+                mix_frame<FW>(v, P.mix1 & MW, P.c1.t);
+            } else {
+                xch<FX, FY>(v, sm, lane, warp);
+                mix_frame<FY>(v, P.mix1 & MY, P.c1.t);
+                xch<FY, FZ>(v, sm, lane, warp);
+                mix_frame<FZ>(v, P.mix1 & MZ, P.c1.t);
             }
-        }
-        if (need_e && warp == 0)
-            tile_tables_warp<2>(tt, sh, sJ, n, P.L, P.lmask, tb | P.xglob, lane, P.phase, P.gamma,
-                                P.scale);
-        if (!P.init) {
-            mix_frame<0>(v, P.mix1, P.c1);
-            xch<0, 1>(v, sm, lane, warp);
-            mix_frame<1>(v, P.mix1, P.c1);
-            xch<1, 2>(v, sm, lane, warp);
-            mix_frame<2>(v, P.mix1, P.c1);
         } else {
 #pragma unroll
             for (int j = 0; j < NR; ++j) v[j] = make_double2(P.a0, 0.0);
-            __syncthreads();  // tables visible
         }
-        if (P.phase) {
-            apply_phase<2>(v, tt, lane, warp, uTT, u);
-            mix_frame<2>(v, P.mix2, P.c2);
-            xch<2, 1>(v, sm, lane, warp);
-            mix_frame<1>(v, P.mix2, P.c2);
-            xch<1, 0>(v, sm, lane, warp);
-            mix_frame<0>(v, P.mix2, P.c2);
-            double2 *dst = P.psi + tb + offA;
-#pragma unroll
-            for (int j = 0; j < NR; ++j) {
-                const u64 o = ((j & 1) ? sA0 : 0) + ((j & 2) ? sA1 : 0) + ((j & 4) ? sA2 : 0) +
-                              ((j & 8) ? sA3 : 0);
-                __stcs(dst + o, v[j]);
+        if (TURN) {
+            apply_phase<FE>(v, R, tE, fr, pconst, u, cs.PRR);
+            if (RUN) {
+                mix_frame<FW>(v, P.mix2 & MW, P.c2.t);
+                xch<FW, FX>(v, sm, lane, warp);
+            } else {
+                mix_frame<FZ>(v, P.mix2 & MZ, P.c2.t);
+                xch<FZ, FY>(v, sm, lane, warp);
+                mix_frame<FY>(v, P.mix2 & MY, P.c2.t);
+                xch<FY, FX>(v, sm, lane, warp);
             }
+            mix_frame<FX>(v, P.mix2 & MX, P.c2.t);
+            store_tile<FX>(v, P.psi + tb + offX, P.L);
         } else {
             if (P.scale.x != 1.0 || P.scale.y != 0.0) {
 #pragma unroll
                 for (int j = 0; j < NR; ++j) v[j] = cmul(v[j], P.scale);
             }
-            if (P.reduce) accumulate<2>(v, tt, lane, warp, te, acc_e, acc_n);
-            double2 *dst = P.psi + tb + offC;
-#pragma unroll
-            for (int j = 0; j < NR; ++j) {
-                const u64 o = ((j & 1) ? sC0 : 0) + ((j & 2) ? sC1 : 0) + ((j & 4) ? sC2 : 0) +
-                              ((j & 8) ? sC3 : 0);
-                __stcs(dst + o, v[j]);
-            }
+            if (P.reduce) accumulate<FE>(v, R, tE, fr, te, cs.eRR, acc_e, acc_n);
+            store_tile<RUN ? FW : FZ>(v, P.psi + tb + offS, P.L);
         }
     }
-    if (P.reduce) block_reduce2(tt, acc_e, acc_n, lane, warp, P.part + 2 * blockIdx.x);
+    if (P.reduce) block_reduce2(cs, acc_e, acc_n, lane, warp, P.part + 2 * blockIdx.x);
 }
 
-// ============================================================ standalone reduction (frame A)
+// ============================================================ standalone reduction (frame X)
 __global__ void __launch_bounds__(NTHR, 2) reduce_kernel(const PassParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileTables &tt = *reinterpret_cast<TileTables *>(smem_raw + SmemLayout::tile);
-    double *sh = reinterpret_cast<double *>(smem_raw + SmemLayout::tile +
-                                            ((SmemLayout::tables + 15) / 16) * 16);
-    double *sJ = sh + NMAX;
+    CtaShared &cs = *reinterpret_cast<CtaShared *>(smem_raw + SmemLayout::tile);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = P.n;
-    load_hj(sh, sJ, P.hp, P.Jp, n);
+    const TileRec *recs = reinterpret_cast<const TileRec *>(P.rec);
+    int ft = 0;
+#pragma unroll
+    for (int i = 0; i < KT; ++i) ft |= (int)((P.flip >> P.L[i]) & 1ull) << i;
+    const int tX = Frame<FX>::tthr(lane, warp) ^ ft;
+    const int fr = (ft >> Frame<FX>::RB) & 0x1F;
+    const ThreadEnergy te = thread_energy<FX>(P.Jp, n, P.L, lane, warp, ft);
+    if (tid < NR) cs.eRR[tid] = err_of<FX>(P.Jp, n, P.L, tid ^ fr);
     __syncthreads();
-    const ThreadEnergy te = thread_energy<0>(sJ, n, P.L, lane, warp);
-    if (tid < 16) tt.eRR[tid] = err_of<0>(sJ, n, P.L, tid);
-    const u64 offA = thread_offset<0>(P.L, lane, warp);
-    const u64 sA0 = 1ull << P.L[8], sA1 = 1ull << P.L[9], sA2 = 1ull << P.L[10], sA3 = 1ull << P.L[11];
+    const u64 offX = thread_offset<FX>(P.L, lane, warp);
     double acc_e = 0.0, acc_n = 0.0;
     double2 v[NR];
     for (u64 ut = blockIdx.x; ut < P.ntiles; ut += gridDim.x) {
-        __syncthreads();
         const u64 tb = tile_base(P, ut);
-        const double2 *src = P.psi + tb + offA;
-#pragma unroll
-        for (int j = 0; j < NR; ++j) {
-            const u64 o = ((j & 1) ? sA0 : 0) + ((j & 2) ? sA1 : 0) + ((j & 4) ? sA2 : 0) +
-                          ((j & 8) ? sA3 : 0);
-            v[j] = __ldcs(src + o);
-        }
-        if (warp == 0)
-            tile_tables_warp<0>(tt, sh, sJ, n, P.L, P.lmask, tb | P.xglob, lane, false, 0.0,
-                                make_double2(1.0, 0.0));
-        __syncthreads();
-        accumulate<0>(v, tt, lane, warp, te, acc_e, acc_n);
+        prefetch_next(P, ut + gridDim.x, tid);
+        load_tile<FX>(v, P.psi + tb + offX, P.L);
+        accumulate<FX>(v, recs + ut, tX, fr, te, cs.eRR, acc_e, acc_n);
     }
-    block_reduce2(tt, acc_e, acc_n, lane, warp, P.part + 2 * blockIdx.x);
+    block_reduce2(cs, acc_e, acc_n, lane, warp, P.part + 2 * blockIdx.x);
 }
 
 // sum the per-CTA partials in a fixed order
@@ -268,7 +303,7 @@ __device__ __forceinline__ u64 logical_to_physical(u64 z, const GatherParams &G)
 __global__ void gather_kernel(const GatherParams G, const double2 *psi, double2 *out) {
     for (u64 k = blockIdx.x * (u64)blockDim.x + threadIdx.x; k < G.count; k += (u64)gridDim.x * blockDim.x) {
         const u64 z = G.list ? G.list[k] : G.first + k;
-        const u64 x = logical_to_physical(z, G);
+        const u64 x = logical_to_physical(z, G) ^ G.flip;
         out[k] = ((x >> G.m) == G.rank) ? psi[x & ((1ull << G.m) - 1ull)] : make_double2(0.0, 0.0);
     }
 }
@@ -285,8 +320,14 @@ __global__ void energy_probe_kernel(const GatherParams G, const double *hp, cons
 size_t pass_smem_bytes() { return SmemLayout::total; }
 
 cudaError_t setup_kernels() {
-    cudaError_t e = cudaFuncSetAttribute(pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SmemLayout::total);
+    cudaError_t e;
+    e = cudaFuncSetAttribute(pass_kernel<K_PLAIN12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmemLayout::total);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(pass_kernel<K_PLAIN_RUN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmemLayout::total);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(pass_kernel<K_TURN12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmemLayout::total);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(pass_kernel<K_TURN_RUN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmemLayout::total);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)SmemLayout::total);
@@ -295,7 +336,19 @@ cudaError_t setup_kernels() {
 }
 
 cudaError_t launch_pass(const PassParams &P, int grid, cudaStream_t s) {
-    pass_kernel<<<grid, NTHR, SmemLayout::total, s>>>(P);
+    switch (P.kind) {
+        case K_PLAIN12: pass_kernel<K_PLAIN12><<<grid, NTHR, SmemLayout::total, s>>>(P); break;
+        case K_PLAIN_RUN: pass_kernel<K_PLAIN_RUN><<<grid, NTHR, SmemLayout::total, s>>>(P); break;
+        case K_TURN12: pass_kernel<K_TURN12><<<grid, NTHR, SmemLayout::total, s>>>(P); break;
+        case K_TURN_RUN: pass_kernel<K_TURN_RUN><<<grid, NTHR, SmemLayout::total, s>>>(P); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_fields(const PassParams &P, void *rec, cudaStream_t s) {
+    int grid = (int)std::min<u64>((P.ntiles + 127) / 128, 8192);
+    tile_fields_kernel<<<grid, 128, 0, s>>>(P, reinterpret_cast<TileRec *>(rec));
     return cudaGetLastError();
 }
 

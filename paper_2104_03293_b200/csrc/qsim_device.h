@@ -10,22 +10,32 @@ namespace qk {
 typedef unsigned long long u64;
 constexpr int KT = 12;          // tile bits per pass
 constexpr int TILE = 1 << KT;   // amplitudes per tile
-constexpr int NTHR = 256;       // threads per CTA
-constexpr int NR = 16;          // amplitudes per thread
+constexpr int NTHR = 128;       // threads per CTA (one tile in flight per CTA)
+constexpr int NR = 32;          // amplitudes per thread (5 register bits)
 constexpr int NMAX = 40;        // max qubits
 constexpr int SM_TILE_BYTES = TILE * 16;
 
 struct Mix {
-    double t;   // tan(beta) (form 0) or -cot(beta) (form 1)
-    int form;
+    double t;   // tan(beta), or -cot(beta) when |tan beta| > 1 (then the X gates go to the flip mask)
+    int form;   // 1 in the latter case (host bookkeeping only)
+};
+
+// pass programs: which register frames a tile visits
+enum PassKind {
+    K_PLAIN12 = 0,   // 12-bit set (bits 0..11), mix1 only:        X -> Y -> Z, store Z
+    K_PLAIN_RUN = 1, // run set (passengers + <= 9 mixed), mix1:    X -> W, store W
+    K_TURN12 = 2,    // 12-bit set, mix1 -> phase -> mix2:          X -> Y -> Z(phase) -> Y -> X
+    K_TURN_RUN = 3   // run set, mix1 -> phase -> mix2:             X -> W(phase) -> X
 };
 
 struct PassParams {
+    int kind;            // PassKind
     double2 *psi;        // local shard, 2^m amplitudes
     const double *hp;    // physical-frame fields, n
     const double *Jp;    // physical-frame couplings, n*n symmetric, zero diagonal
     int n, m;
     u64 xglob;           // global (rank) bits placed at positions m..n-1
+    u64 flip;            // index flip mask F for the energies of this pass (psi_{x^F} stored at x)
     u64 lmask;           // mask of the tile-bit positions
     int L[KT];           // tile-bit positions (ascending)
     int nseg;            // complement segments: tile id bits -> physical positions
@@ -39,7 +49,11 @@ struct PassParams {
     double a0;           // 2^(-n/2)
     double gamma;
     double *part;        // reduce partials, 2 per CTA
+    const void *rec;     // per-tile records (TileRec), written by tile_fields_kernel
+    int prefetch;        // L2-prefetch the CTA's next tile
 };
+
+constexpr size_t TILE_REC_BYTES = 320;  // sizeof(TileRec)
 
 struct SmallParams {
     double2 *psi;
@@ -53,6 +67,7 @@ struct SmallParams {
 struct GatherParams {
     int n, m;
     u64 rank;
+    u64 flip;            // physical index flip mask
     u64 first, count;
     const u64 *list;     // optional explicit logical labels (device)
     unsigned char pos[NMAX];
@@ -67,6 +82,7 @@ struct ProbeSet {
 size_t pass_smem_bytes();
 cudaError_t setup_kernels();
 cudaError_t launch_pass(const PassParams &P, int grid, cudaStream_t s);
+cudaError_t launch_tile_fields(const PassParams &P, void *rec, cudaStream_t s);
 cudaError_t launch_reduce(const PassParams &P, int grid, cudaStream_t s);
 cudaError_t launch_sum_partials(const double *part, int nparts, double *res, cudaStream_t s);
 cudaError_t launch_small(const SmallParams &P, cudaStream_t s);

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -31,6 +32,7 @@ struct TileSet {
     int L[qk::KT];
     u64 lmask;
     unsigned own;  // tile-bit mask of the bits this set mixes
+    bool full12;   // the 12-bit set of bits 0..11 (all mixed) vs a "run" set with passengers
     int nseg;
     int seg_len[8], seg_dst[8];
     u64 ntiles;
@@ -83,23 +85,35 @@ std::vector<TileSet> build_sets(int m) {
     std::vector<int> L0(qk::KT);
     for (int i = 0; i < qk::KT; ++i) L0[i] = i;
     sets.push_back(make_set(m, L0, (1u << qk::KT) - 1));
+    sets.back().full12 = true;
     for (auto &r : runs) {
         std::vector<int> L;
         int npass = qk::KT - r.second;
         for (int i = 0; i < npass; ++i) L.push_back(i);
         for (int i = 0; i < r.second; ++i) L.push_back(r.first + i);
         sets.push_back(make_set(m, L, ((1u << r.second) - 1) << npass));
+        sets.back().full12 = false;
     }
     return sets;
 }
 
-// pass schedule for p layers (see file header); `first_init` fuses |+>^n into pass 0
+// pass schedule for p layers; `first_init` fuses |+>^n into pass 0.
+// One GPU: boustrophedon over the set order [R_1, S_12, R_2, ..., R_{P-1}] (the 12-bit
+// set sits in the middle, so every phase-carrying "turning" pass is a run set); the
+// pass on the last set of layer k also does phase_{k+1} and the first mix of layer k+1:
+// (P-1) p + 1 passes.  G > 1: fixed schedule, top run first (boundary pass: arrivals
+// with beta_{k-1}, phase_k, set with beta_k), the other sets, then the swap of the top
+// g local bits with the global bits: P p + 1 passes, p swaps.
 std::vector<PassOp> build_schedule(int nsets, int g, int p, const double *gam, const double *bet,
                                    bool first_init) {
     std::vector<PassOp> ops;
     const int P = nsets;
     if (g == 0) {
-        auto seq = [&](int k, int idx) { return (k % 2 == 0) ? idx : P - 1 - idx; };
+        std::vector<int> order;
+        order.push_back(P > 1 ? 1 : 0);
+        if (P > 1) order.push_back(0);
+        for (int i = 2; i < P; ++i) order.push_back(i);
+        auto seq = [&](int k, int idx) { return order[(k % 2 == 0) ? idx : P - 1 - idx]; };
         ops.push_back({seq(0, 0), first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false});
         for (int k = 0; k < p; ++k) {
             for (int idx = 1; idx < P; ++idx) {
@@ -178,15 +192,18 @@ struct qsim {
     bool has_ising = false;
     std::vector<double> h, J;  // logical, J symmetric with zero diagonal
     int parity = 0;            // number of swaps mod 2 (permutation state)
+    u64 flip = 0;              // index flip mask F: physical x holds the amplitude of x ^ F
     double *d_hp[2] = {nullptr, nullptr}, *d_Jp[2] = {nullptr, nullptr};
     double *d_part = nullptr, *d_res = nullptr, *d_ang = nullptr;
     size_t ang_cap = 0;
     void *d_scratch = nullptr;
     size_t scratch_cap = 0;
+    void *d_rec = nullptr;     // per-tile records of the current pass (tile_fields_kernel)
     std::vector<TileSet> sets;
     bool pending_plus = true;
     bool res_valid = false;
     uint64_t launches = 0;
+    int prefetch = 1;          // L2 prefetch of the next tile (QSIM_PREFETCH=0 disables, for experiments)
     std::string err;
     // optional per-pass timing (CUDA events on the handle's stream around each pass launch)
     bool prof = false;
@@ -246,6 +263,7 @@ int materialize_plus(qsim *q) {
     CK(qk::launch_init_plus(q->psi, 1ull << q->m, a0, q->num_sms * 8, q->st));
     q->launches++;
     q->pending_plus = false;
+    q->flip = 0;
     q->res_valid = false;
     return QSIM_OK;
 }
@@ -269,6 +287,9 @@ qk::PassParams base_params(qsim *q, const TileSet &S) {
     P.a0 = std::pow(2.0, -0.5 * q->n);
     P.part = q->d_part;
     P.scale = make_double2(1.0, 0.0);
+    // L2 prefetch pays only for the contiguous 64 KiB tiles of the 12-bit set; for run sets
+    // every tile touches up to 512 distinct 2 MiB pages and prefetching slows them (measured)
+    P.prefetch = q->prefetch && S.full12;
     return P;
 }
 
@@ -283,6 +304,12 @@ int finish_reduce(qsim *q, int nparts) {
 // global-qubit swap: positions [m-g, m) <-> [m, n); rank r's chunk c <-> rank c's chunk r
 int do_swap(qsim *q) {
     const int G = q->world;
+    {   // the flip mask travels with the qubits: positions [m-g, m) <-> [m, n)
+        const u64 gm = (1ull << q->g) - 1ull;
+        const u64 lo = (q->flip >> (q->m - q->g)) & gm, hi = (q->flip >> q->m) & gm;
+        q->flip &= ~((gm << (q->m - q->g)) | (gm << q->m));
+        q->flip |= (hi << (q->m - q->g)) | (lo << q->m);
+    }
     const u64 chunk = 1ull << (q->m - q->g);  // amplitudes per chunk
     const size_t cbytes = chunk * sizeof(double2);
     if (q->tmp) {
@@ -386,6 +413,7 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         return QSIM_OK;
     }
     std::vector<PassOp> ops = build_schedule((int)q->sets.size(), q->g, p, gam, bet, q->pending_plus);
+    if (q->pending_plus) q->flip = 0;
     int last_grid = 0;
     for (const PassOp &op : ops) {
         const TileSet &S = q->sets[op.set];
@@ -398,10 +426,28 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         P.mix2 = op.phase ? m2 : 0u;
         std::complex<double> sc = cpow_int(k1, __builtin_popcount(P.mix1)) * cpow_int(k2, __builtin_popcount(P.mix2));
         P.scale = make_double2(sc.real(), sc.imag());
+        // X gates of the |tan beta| > 1 form -> flip mask (energies of this pass use the
+        // mask after mix1; the state after the pass carries the mask after mix2)
+        auto posmask = [&](unsigned tm) {
+            u64 r = 0;
+            for (int i = 0; i < qk::KT; ++i)
+                if ((tm >> i) & 1u) r |= 1ull << S.L[i];
+            return r;
+        };
+        const u64 f1 = P.c1.form ? posmask(P.mix1) : 0ull;
+        const u64 f2 = P.c2.form ? posmask(P.mix2) : 0ull;
+        P.flip = q->flip ^ f1;
+        q->flip = P.flip ^ f2;
+        P.kind = S.full12 ? (op.phase ? qk::K_TURN12 : qk::K_PLAIN12) : (op.phase ? qk::K_TURN_RUN : qk::K_PLAIN_RUN);
         P.init = op.init;
         P.phase = op.phase;
         P.reduce = op.reduce;
         P.gamma = op.gamma;
+        P.rec = q->d_rec;
+        if (op.phase || op.reduce) {
+            CK(qk::launch_tile_fields(P, q->d_rec, q->st));
+            q->launches++;
+        }
         int grid = grid_for(q, S.ntiles);
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (q->prof) {
@@ -454,6 +500,10 @@ int run_reduce(qsim *q) {
     }
     const TileSet &S = q->sets[0];
     qk::PassParams P = base_params(q, S);
+    P.rec = q->d_rec;
+    P.flip = q->flip;
+    CK(qk::launch_tile_fields(P, q->d_rec, q->st));
+    q->launches++;
     int grid = grid_for(q, S.ntiles);
     CK(qk::launch_reduce(P, grid, q->st));
     q->launches++;
@@ -468,6 +518,7 @@ qk::GatherParams gather_params(const qsim *q, u64 first, u64 count, const u64 *l
     G.first = first;
     G.count = count;
     G.list = list;
+    G.flip = q->flip;
     for (int b = 0; b < q->n; ++b) G.pos[b] = (unsigned char)phys_pos(q->n, q->m, q->g, q->parity, b);
     return G;
 }
@@ -540,7 +591,10 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     }
     CK(cudaMalloc(&q->d_part, sizeof(double) * 2 * 4 * q->num_sms));
     CK(cudaMalloc(&q->d_res, sizeof(double) * 2));
-    if (q->m > qk::KT) q->sets = build_sets(q->m);
+    if (q->m > qk::KT) {
+        q->sets = build_sets(q->m);
+        CK(cudaMalloc(&q->d_rec, qk::TILE_REC_BYTES << (q->m - qk::KT)));
+    }
     if (world > 1) {
         ncclUniqueId id;
         std::memcpy(&id, uid, sizeof(id));
@@ -556,6 +610,7 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
         }
     }
     q->pending_plus = true;
+    if (const char *e = std::getenv("QSIM_PREFETCH")) q->prefetch = std::atoi(e);
     return QSIM_OK;
 }
 
@@ -598,6 +653,7 @@ int qsim_destroy(qsim_t *q) {
     if (q->d_res) cudaFree(q->d_res);
     if (q->d_ang) cudaFree(q->d_ang);
     if (q->d_scratch) cudaFree(q->d_scratch);
+    if (q->d_rec) cudaFree(q->d_rec);
     for (cudaEvent_t e : q->ev_pool) cudaEventDestroy(e);
     if (q->own_stream && q->st) cudaStreamDestroy(q->st);
     delete q;
@@ -782,6 +838,45 @@ int qsim_plan_positions(int n, int world, int layers, int *pos_out) {
     if (n < 1 || n > qk::NMAX || g < 0 || world > 8 || layers < 0 || !pos_out) return QSIM_EINVAL;
     int m = n - g;
     for (int qb = 0; qb < n; ++qb) pos_out[qb] = phys_pos(n, m, g, layers & 1, qb);
+    return QSIM_OK;
+}
+
+int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
+    if (!q || !ms_out || reps < 1) return QSIM_EINVAL;
+    if (q->m <= qk::KT || set < 0 || set >= (int)q->sets.size()) return fail(q, QSIM_EINVAL, "no such tile set");
+    if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
+    int rc = materialize_plus(q);
+    if (rc) return rc;
+    const TileSet &S = q->sets[set];
+    qk::PassParams P = base_params(q, S);
+    std::complex<double> k1, k2;
+    P.c1 = mix_coef(0.3, k1);
+    P.c2 = mix_coef(-0.2, k2);
+    P.mix1 = S.own;
+    P.mix2 = phase ? S.own : 0u;
+    std::complex<double> sc = cpow_int(k1, __builtin_popcount(P.mix1)) * cpow_int(k2, __builtin_popcount(P.mix2));
+    P.scale = make_double2(sc.real(), sc.imag());
+    P.kind = S.full12 ? (phase ? qk::K_TURN12 : qk::K_PLAIN12) : (phase ? qk::K_TURN_RUN : qk::K_PLAIN_RUN);
+    P.phase = phase;
+    P.gamma = 0.1;
+    P.rec = q->d_rec;
+    P.flip = q->flip;
+    CK(qk::launch_tile_fields(P, q->d_rec, q->st));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    int grid = grid_for(q, S.ntiles);
+    CK(qk::launch_pass(P, grid, q->st));  // warm-up
+    CK(cudaEventRecord(e0, q->st));
+    for (int r = 0; r < reps; ++r) CK(qk::launch_pass(P, grid, q->st));
+    CK(cudaEventRecord(e1, q->st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    q->res_valid = false;
+    *ms_out = ms / reps;
     return QSIM_OK;
 }
 

@@ -1,25 +1,23 @@
 // qsim_kernels.cuh -- sm_100a device code of the QAOA / AQA hot path
 // (arXiv:2104.03293).
 //
-// One "tile pass" streams the local shard through HBM once: each CTA owns tiles of
-// 2^12 amplitudes whose 12 "tile bits" sit at physical bit positions L[0..11]
-// (ascending); for every tile it
-//   (load)   reads the tile straight into registers (16 amplitudes per thread, frame A,
-//            warp lanes on the lowest tile bits -> >= 128-byte coalesced runs),
-//   (mix)    applies e^{-i beta sigma^x} to the tile bits in `mix1` as 2x2 butterflies
-//            (eq:twocomponentupdates) on register bits, re-distributing the
-//            tile between three register frames A -> B -> C through shared memory,
-//   (phase)  optionally multiplies psi_z by e^{-i gamma E(z)} (eq:QAOA_state) with E(z)
-//            evaluated on the fly by the tile factorisation of SURVEY §8a-a4
-//            (no 2^n energy table), then mixes the bits in `mix2` (C -> B -> A),
-//   (reduce) optionally accumulates sum |psi|^2 E(z) and sum |psi|^2,
-//   (store)  writes the tile back in place (frame C or A, coalesced).
-// An `init` pass synthesises |+>^n instead of loading (write-only pass).
+// One "tile pass" streams the local shard through HBM once.  A CTA of 128 threads owns
+// one tile of 2^12 amplitudes at a time (32 per thread, held in registers); the tile's
+// 12 "tile bits" t0..t11 sit at physical bit positions L[0..11] (ascending).  Per tile:
+//   (load)   straight into registers, frame X (lanes on t0..t4 -> coalesced runs),
+//   (mix)    e^{-i beta sigma^x} on the tile bits in `mix1` as 2x2 butterflies on
+//            register bits (eq:twocomponentupdates); the tile moves between
+//            register frames through a swizzled 64 KiB shared-memory buffer,
+//   (phase)  optionally psi_z *= e^{-i gamma E(z)} (eq:QAOA_state), E(z) from the tile
+//            factorisation of SURVEY §8a-a4 (per-tile fields precomputed by
+//            tile_fields_kernel, no 2^n energy table), then mixes the bits in `mix2`,
+//   (reduce) optionally accumulates sum |psi|^2 E(z), sum |psi|^2,
+//   (store)  back in place from a coalesced frame.
 //
-// Scaled butterflies: e^{-i b X} = cos b (I - i tan b X)  (|cos b| >= |sin b|, form 0)
-//                              = -i sin b (X - i(-cot b) ... ) (form 1, see mix_bfly),
-// so each butterfly costs 2 FMA per output amplitude; the pass-wide scalar
-// kappa^m is folded into the phase factor (or applied once per amplitude).
+// Scaled butterflies: e^{-i b X} = cos b (I - i tan b X) when |cos b| >= |sin b|, and
+// (-i X) e^{-i (b - pi/2) X} otherwise (the X gates become an index flip mask, see bfly):
+// 2 FMA per output amplitude; the pass-wide scalar kappa^m is folded into the phase (or
+// applied once per amplitude).
 //
 // No code here is shared with oracle/ (the CPU oracle is independent).
 #pragma once
@@ -45,17 +43,19 @@ __device__ __forceinline__ double2 expmi(double theta) {
     return make_double2(c, -s);
 }
 
-// shared-memory swizzle for 16-byte elements: conflict-free LDS/STS.128 in frames A, B, C
-__device__ __forceinline__ int swz(int t) { return t ^ ((t >> 4) & 7); }
+// shared-memory swizzle for 16-byte elements: conflict-free LDS/STS.128 in all frames
+// (every quarter-warp varies t0..t2 or t5..t7, and the XOR mixes exactly those).
+__device__ __forceinline__ int swz(int t) { return t ^ ((t >> 5) & 7); }
 
 // ------------------------------------------------------------------ energy arithmetic
-// Tile factorisation of E(z).  With the tile bits L and the other
-// bits H (local non-tile + global):
+// Tile factorisation of E(z).  With the tile bits L and the other bits
+// H (local non-tile + global):
 //   E = E_H(z_H) + sum_{i in L} s_i h'_i(z_H) + E_LL(z_L),
-//   h'_i(z_H) = h_i + sum_{j in H} J_ij s_j,  E_H = sum_{j in H} s_j (h_j + sum_{k in H, k>j} J_jk s_k).
-// Every partial sum of dyadic data is exact, so E is bit-exact independent of order.
-// These two functions are the single source of that arithmetic for the pass, reduce
-// and probe kernels.
+//   h'_i(z_H) = h_i + sum_{j in H} J_ij s_j,
+//   E_H = sum_{j in H} s_j (h_j + sum_{k in H, k>j} J_jk s_k).
+// Every partial sum of dyadic data is exact, so E is bit-exact in any order.  These
+// two functions are the single source of that arithmetic for the tile-field, pass,
+// reduce and probe kernels.
 __device__ __forceinline__ double field_hprime(const double *hp, const double *Jp, int n, int pos,
                                                u64 X, u64 lmask) {
     const double *row = Jp + pos * n;
@@ -88,72 +88,63 @@ __device__ double energy_point(const double *hp, const double *Jp, int n, const 
 }
 
 // ------------------------------------------------------------------------ register frames
-// tile index t (12 bits) of register j held by (lane, warp):
-//   A: lanes t0..t4, warps t5..t7, regs t8..t11     (load / turning-pass store)
-//   B: regs  t0..t3, lanes t4..t8, warps t9..t11
-//   C: lanes t0..t3,t8, regs t4..t7, warps t9..t11  (phase, reduce, plain-pass store)
+// Tile index t (12 bits) of register j (5 bits) held by (lane, warp); the register bits
+// are always the contiguous tile bits RB..RB+4:  t = tthr(lane, warp) | (j << RB).
+//   X: lanes t0..t4,          warps t5,t6,   regs t7..t11   (load; turning-pass store)
+//   Y: lanes t5..t9,          warps t10,t11, regs t0..t4
+//   Z: lanes t0..t4,          warps t10,t11, regs t5..t9    (12-bit phase / store)
+//   W: lanes t0,t1,t2,t8,t9,  warps t10,t11, regs t3..t7    (run phase / store)
+enum { FX = 0, FY = 1, FZ = 2, FW = 3 };
 template <int F> struct Frame;
-template <> struct Frame<0> {
-    static constexpr int RB = 8;
+template <> struct Frame<FX> {
+    static constexpr int RB = 7;
     __device__ static int tthr(int lane, int warp) { return lane | (warp << 5); }
-    __host__ __device__ static constexpr int lbit(int b) { return b; }
-    __host__ __device__ static constexpr int wbit(int b) { return 5 + b; }
 };
-template <> struct Frame<1> {
+template <> struct Frame<FY> {
     static constexpr int RB = 0;
-    __device__ static int tthr(int lane, int warp) { return (lane << 4) | (warp << 9); }
-    __host__ __device__ static constexpr int lbit(int b) { return 4 + b; }
-    __host__ __device__ static constexpr int wbit(int b) { return 9 + b; }
+    __device__ static int tthr(int lane, int warp) { return (lane << 5) | (warp << 10); }
 };
-template <> struct Frame<2> {
-    static constexpr int RB = 4;
+template <> struct Frame<FZ> {
+    static constexpr int RB = 5;
+    __device__ static int tthr(int lane, int warp) { return lane | (warp << 10); }
+};
+template <> struct Frame<FW> {
+    static constexpr int RB = 3;
     __device__ static int tthr(int lane, int warp) {
-        return (lane & 15) | ((lane >> 4) << 8) | (warp << 9);
+        return (lane & 7) | ((lane >> 3) << 8) | (warp << 10);
     }
-    __host__ __device__ static constexpr int lbit(int b) { return b < 4 ? b : 8; }
-    __host__ __device__ static constexpr int wbit(int b) { return 9 + b; }
 };
 
 // ------------------------------------------------------------------------- butterflies
-// form 0: (a, b) <- (a - i t b, b - i t a)           [e^{-i b X} / cos b, t = tan b]
-// form 1: (a, b) <- (b - i t a, a - i t b)           [e^{-i b X} / (-i sin b), t = -cot b]
-template <int RBIT, bool FORM1>
+// (a, b) <- (a - i t b, b - i t a) = e^{-i beta X} / cos(beta) with t = tan(beta).
+// For |tan beta| > 1 the host uses e^{-i beta X} = (-i X) e^{-i (beta - pi/2) X}
+// (t = -cot beta, kappa = -i sin beta): the X gates commute with every mixer and are
+// tracked as an index flip mask F (state holds psi_{x xor F} at physical index x), so
+// there is one butterfly form and no data movement for them.
+template <int RBIT>
 __device__ __forceinline__ void bfly(double2 (&v)[NR], double t) {
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
         if (j & (1 << RBIT)) continue;
         const double2 a = v[j], b = v[j | (1 << RBIT)];
-        const double2 x = make_double2(fma(t, b.y, a.x), fma(-t, b.x, a.y));
-        const double2 y = make_double2(fma(t, a.y, b.x), fma(-t, a.x, b.y));
-        if (FORM1) {
-            v[j] = y;
-            v[j | (1 << RBIT)] = x;
-        } else {
-            v[j] = x;
-            v[j | (1 << RBIT)] = y;
-        }
+        v[j] = make_double2(fma(t, b.y, a.x), fma(-t, b.x, a.y));
+        v[j | (1 << RBIT)] = make_double2(fma(t, a.y, b.x), fma(-t, a.x, b.y));
     }
 }
 
+// mix the tile bits of `mask` that are register bits of frame F
 template <int F>
-__device__ __forceinline__ void mix_frame(double2 (&v)[NR], unsigned mask, Mix c) {
-    const unsigned m4 = (mask >> Frame<F>::RB) & 0xFu;
-    if (!m4) return;
-    if (c.form) {
-        if (m4 & 1) bfly<0, true>(v, c.t);
-        if (m4 & 2) bfly<1, true>(v, c.t);
-        if (m4 & 4) bfly<2, true>(v, c.t);
-        if (m4 & 8) bfly<3, true>(v, c.t);
-    } else {
-        if (m4 & 1) bfly<0, false>(v, c.t);
-        if (m4 & 2) bfly<1, false>(v, c.t);
-        if (m4 & 4) bfly<2, false>(v, c.t);
-        if (m4 & 8) bfly<3, false>(v, c.t);
-    }
+__device__ __forceinline__ void mix_frame(double2 (&v)[NR], unsigned mask, double t) {
+    const unsigned m5 = (mask >> Frame<F>::RB) & 0x1Fu;
+    if (m5 & 1) bfly<0>(v, t);
+    if (m5 & 2) bfly<1>(v, t);
+    if (m5 & 4) bfly<2>(v, t);
+    if (m5 & 8) bfly<3>(v, t);
+    if (m5 & 16) bfly<4>(v, t);
 }
 
 // frame change through shared memory (one barrier); every thread writes back exactly
-// the elements it read in the previous exchange, so only the single barrier is needed.
+// the elements it read in the previous exchange, so one barrier per exchange suffices.
 template <int F1, int F2>
 __device__ __forceinline__ void xch(double2 (&v)[NR], double2 *sm, int lane, int warp) {
     const int t1 = Frame<F1>::tthr(lane, warp);
@@ -176,6 +167,30 @@ __device__ __forceinline__ u64 thread_offset(const int *L, int lane, int warp) {
     return off;
 }
 
+template <int F>
+__device__ __forceinline__ void load_tile(double2 (&v)[NR], const double2 *base, const int *L) {
+    const u64 s0 = 1ull << L[Frame<F>::RB], s1 = 1ull << L[Frame<F>::RB + 1], s2 = 1ull << L[Frame<F>::RB + 2],
+              s3 = 1ull << L[Frame<F>::RB + 3], s4 = 1ull << L[Frame<F>::RB + 4];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+        const u64 o = ((j & 1) ? s0 : 0) + ((j & 2) ? s1 : 0) + ((j & 4) ? s2 : 0) + ((j & 8) ? s3 : 0) +
+                      ((j & 16) ? s4 : 0);
+        v[j] = __ldcs(base + o);
+    }
+}
+
+template <int F>
+__device__ __forceinline__ void store_tile(const double2 (&v)[NR], double2 *base, const int *L) {
+    const u64 s0 = 1ull << L[Frame<F>::RB], s1 = 1ull << L[Frame<F>::RB + 1], s2 = 1ull << L[Frame<F>::RB + 2],
+              s3 = 1ull << L[Frame<F>::RB + 3], s4 = 1ull << L[Frame<F>::RB + 4];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+        const u64 o = ((j & 1) ? s0 : 0) + ((j & 2) ? s1 : 0) + ((j & 4) ? s2 : 0) + ((j & 8) ? s3 : 0) +
+                      ((j & 16) ? s4 : 0);
+        __stcs(base + o, v[j]);
+    }
+}
+
 __device__ __forceinline__ u64 tile_base(const PassParams &P, u64 u) {
     u64 off = 0;
     int src = 0;
@@ -191,13 +206,13 @@ __device__ __forceinline__ u64 tile_base(const PassParams &P, u64 u) {
 //   eTT = sum_{i<i' in T} J s_i s_i',  w_r = sum_{i in T} J_{R_r, i} s_i
 struct ThreadEnergy {
     double eTT;
-    double w[4];
+    double w[5];
 };
 
 template <int F>
-__device__ ThreadEnergy thread_energy(const double *Jp, int n, const int *L, int lane, int warp) {
-    const int t = Frame<F>::tthr(lane, warp);
-    const unsigned rmask = 0xFu << Frame<F>::RB;
+__device__ ThreadEnergy thread_energy(const double *Jp, int n, const int *L, int lane, int warp, int ft) {
+    const int t = Frame<F>::tthr(lane, warp) ^ ft;  // spins of the flipped index
+    const unsigned rmask = 0x1Fu << Frame<F>::RB;
     ThreadEnergy te;
     te.eTT = 0.0;
     for (int i = 0; i < KT; ++i) {
@@ -210,7 +225,7 @@ __device__ ThreadEnergy thread_energy(const double *Jp, int n, const int *L, int
         }
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < 5; ++r) {
         const int ir = Frame<F>::RB + r;
         double w = 0.0;
         for (int i = 0; i < KT; ++i) {
@@ -222,116 +237,97 @@ __device__ ThreadEnergy thread_energy(const double *Jp, int n, const int *L, int
     return te;
 }
 
-// E_RR(j) = sum_{r<r'} J_{R_r R_r'} s_r(j) s_r'(j) for the 16 register patterns
+// E_RR(j) = sum_{r<r'} J_{R_r R_r'} s_r(j) s_r'(j) for the 32 register patterns
+// (j already xor-ed with the register-bit flips by the caller)
 template <int F>
 __device__ double err_of(const double *Jp, int n, const int *L, int j) {
     double e = 0.0;
-    for (int r = 0; r < 4; ++r)
-        for (int r2 = r + 1; r2 < 4; ++r2)
+    for (int r = 0; r < 5; ++r)
+        for (int r2 = r + 1; r2 < 5; ++r2)
             e += Jp[L[Frame<F>::RB + r] * n + L[Frame<F>::RB + r2]] * (((j >> r) & 1) ? 1.0 : -1.0) *
                  (((j >> r2) & 1) ? 1.0 : -1.0);
     return e;
 }
 
-// shared per-CTA tables (per tile)
-struct TileTables {
-    double hL[KT];       // h'_i of the tile bits
-    double EH;           // E_H(z_H)
-    double2 f[KT + 1];   // e^{-i gamma h'_i}, f[KT] = e^{-i gamma E_H}
-    double2 tabL[32];    // phase product over lane bits
-    double2 tabW[8];     // phase product over warp bits * Phi_H * scale
-    double2 fR[4];       // e^{-i gamma h'_{R_r}}
-    double eL[32];       // energy sum over lane bits
-    double eW[8];        // E_H + energy sum over warp bits
-    double hR[4];        // h' of the register bits
-    double2 PRR[16];     // e^{-i gamma E_RR(j)}   (launch constant)
-    double eRR[16];      // E_RR(j)                (launch constant)
+// per-CTA launch constants and reduction scratch in shared memory
+struct CtaShared {
+    double2 PRR[NR];     // e^{-i gamma E_RR(j)}
+    double eRR[NR];      // E_RR(j)
     double red[2][NTHR / 32];
 };
 
-// warp 0: fields of the tile with base X (bits at L are zero) and the frame-F tables
+// per-tile record written by tile_fields_kernel:
+//   e[i] = h'_i(z_H) for the 12 tile bits, e[12] = E_H(z_H);  f[i] = e^{-i gamma e[i]}
+struct __align__(16) TileRec {
+    double2 f[13];
+    double e[13];
+    double pad;
+};
+
+__device__ __forceinline__ double2 ldg2(const double2 *p) { return __ldg(p); }
+
+// psi_z *= e^{-i gamma E} for the thread's 32 amplitudes (frame F):
+//   E = E_H + sum_{i in T} s_i h'_i + E_TT + sum_r s_r (h'_{R_r} + w_r) + E_RR(j)
+// pconst = kappa-scale * e^{-i gamma E_TT};  u[r] = e^{-i gamma w_r}.
+// The register-bit factor is lo[j & 3] * hi[j >> 2] (conjugate symmetry halves the work).
+// tthr is the thread's tile index xor the tile-bit flips; fr = register-bit flips.
 template <int F>
-__device__ void tile_tables_warp(TileTables &tt, const double *hp, const double *Jp, int n,
-                                 const int *L, u64 lmask, u64 X, int lane, bool do_phase,
-                                 double gamma, double2 scale) {
-    double t = 0.0;
-    for (int j = lane; j < n; j += 32)
-        if (!((lmask >> j) & 1ull)) t += eh_term(hp, Jp, n, j, X, lmask);
+__device__ __forceinline__ void apply_phase(double2 (&v)[NR], const TileRec *R, int tthr, int fr, double2 pconst,
+                                            const double2 (&u)[5], const double2 *PRR) {
+    double2 base = cmul(ldg2(&R->f[12]), pconst);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    double hl = 0.0;
-    if (lane < KT) {
-        hl = field_hprime(hp, Jp, n, L[lane], X, lmask);
-        tt.hL[lane] = hl;
+    for (int i = 0; i < KT; ++i) {
+        if (i >= Frame<F>::RB && i < Frame<F>::RB + 5) continue;
+        const double2 fi = ldg2(&R->f[i]);
+        const double sg = ((tthr >> i) & 1) ? 1.0 : -1.0;
+        base = cmul(base, make_double2(fi.x, sg * fi.y));
     }
-    if (lane == 0) tt.EH = t;
-    if (do_phase) {
-        if (lane < KT) tt.f[lane] = expmi(gamma * hl);
-        if (lane == KT) tt.f[KT] = expmi(gamma * t);
-    }
-    __syncwarp();
-    {   // lane-bit tables
-        double e = 0.0;
-        double2 ph = make_double2(1.0, 0.0);
+    double2 g[5];
 #pragma unroll
-        for (int b = 0; b < 5; ++b) {
-            const int i = Frame<F>::lbit(b);
-            const bool up = (lane >> b) & 1;
-            e += up ? tt.hL[i] : -tt.hL[i];
-            if (do_phase) ph = cmul(ph, up ? tt.f[i] : conjd(tt.f[i]));
-        }
-        tt.eL[lane] = e;
-        if (do_phase) tt.tabL[lane] = ph;
+    for (int r = 0; r < 5; ++r) {
+        const double2 gr = cmul(ldg2(&R->f[Frame<F>::RB + r]), u[r]);
+        g[r] = ((fr >> r) & 1) ? conjd(gr) : gr;  // flipped register bit: s_r -> -s_r
     }
-    if (lane < 8) {
-        double e = tt.EH;
-        double2 ph = do_phase ? cmul(tt.f[KT], scale) : make_double2(1.0, 0.0);
+    // lo over register bits 0,1 (times base): {c(A), B, c(B), A} with A = g0 g1, B = g0 c(g1)
+    const double2 A = cmul(g[0], g[1]), B = cmul(g[0], conjd(g[1]));
+    double2 lo[4];
+    lo[0] = cmul(base, conjd(A));
+    lo[1] = cmul(base, B);
+    lo[2] = cmul(base, conjd(B));
+    lo[3] = cmul(base, A);
+    // hi over register bits 2,3,4: hi[k|4] = h4[k] g4, hi[k] = conj(hi[(3-k)|4])
+    const double2 C = cmul(g[2], g[3]), D = cmul(g[2], conjd(g[3]));
+    double2 hi[8];
+    hi[4] = cmul(conjd(C), g[4]);
+    hi[5] = cmul(D, g[4]);
+    hi[6] = cmul(conjd(D), g[4]);
+    hi[7] = cmul(C, g[4]);
+    hi[0] = conjd(hi[7]);
+    hi[1] = conjd(hi[6]);
+    hi[2] = conjd(hi[5]);
+    hi[3] = conjd(hi[4]);
 #pragma unroll
-        for (int b = 0; b < 3; ++b) {
-            const int i = Frame<F>::wbit(b);
-            const bool up = (lane >> b) & 1;
-            e += up ? tt.hL[i] : -tt.hL[i];
-            if (do_phase) ph = cmul(ph, up ? tt.f[i] : conjd(tt.f[i]));
-        }
-        tt.eW[lane] = e;
-        if (do_phase) tt.tabW[lane] = ph;
-    }
-    if (lane < 4) {
-        tt.hR[lane] = tt.hL[Frame<F>::RB + lane];
-        if (do_phase) tt.fR[lane] = tt.f[Frame<F>::RB + lane];
-    }
+    for (int j = 0; j < NR; ++j) v[j] = cmul(v[j], cmul(cmul(lo[j & 3], hi[j >> 2]), PRR[j]));
 }
 
-// multiply v[j] by e^{-i gamma E} for the thread's 16 amplitudes (frame F)
+// accumulate sum |psi|^2 E and sum |psi|^2 over the thread's 32 amplitudes (frame F)
 template <int F>
-__device__ __forceinline__ void apply_phase(double2 (&v)[NR], const TileTables &tt, int lane,
-                                            int warp, double2 uTT, const double2 (&u)[4]) {
-    double2 P[NR];
-    P[0] = cmul(cmul(tt.tabL[lane], tt.tabW[warp]), uTT);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const double2 g = cmul(tt.fR[r], u[r]);
-        const double2 gc = conjd(g);
-#pragma unroll
-        for (int j = 0; j < (1 << r); ++j) {
-            P[j + (1 << r)] = cmul(P[j], g);
-            P[j] = cmul(P[j], gc);
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < NR; ++j) v[j] = cmul(v[j], cmul(P[j], tt.PRR[j]));
-}
-
-// accumulate sum |psi|^2 E and sum |psi|^2 over the thread's 16 amplitudes (frame F)
-template <int F>
-__device__ __forceinline__ void accumulate(const double2 (&v)[NR], const TileTables &tt, int lane,
-                                           int warp, const ThreadEnergy &te, double &acc_e,
+__device__ __forceinline__ void accumulate(const double2 (&v)[NR], const TileRec *R, int tthr, int fr,
+                                           const ThreadEnergy &te, const double *eRR, double &acc_e,
                                            double &acc_n) {
     double Q[NR];
-    Q[0] = tt.eL[lane] + tt.eW[warp] + te.eTT;
+    double eb = __ldg(&R->e[12]) + te.eTT;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const double a = tt.hR[r] + te.w[r];
+    for (int i = 0; i < KT; ++i) {
+        if (i >= Frame<F>::RB && i < Frame<F>::RB + 5) continue;
+        const double ei = __ldg(&R->e[i]);
+        eb += ((tthr >> i) & 1) ? ei : -ei;
+    }
+    Q[0] = eb;
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+        const double a0 = __ldg(&R->e[Frame<F>::RB + r]) + te.w[r];
+        const double a = ((fr >> r) & 1) ? -a0 : a0;
 #pragma unroll
         for (int j = 0; j < (1 << r); ++j) {
             Q[j + (1 << r)] = Q[j] + a;
@@ -341,12 +337,12 @@ __device__ __forceinline__ void accumulate(const double2 (&v)[NR], const TileTab
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
         const double p = fma(v[j].x, v[j].x, v[j].y * v[j].y);
-        acc_e = fma(p, Q[j] + tt.eRR[j], acc_e);
+        acc_e = fma(p, Q[j] + eRR[j], acc_e);
         acc_n += p;
     }
 }
 
-__device__ __forceinline__ void block_reduce2(TileTables &tt, double a, double b, int lane, int warp,
+__device__ __forceinline__ void block_reduce2(CtaShared &tt, double a, double b, int lane, int warp,
                                               double *out) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) {

@@ -37,7 +37,7 @@ EXPORTS = ["qsim_create", "qsim_create_ex", "qsim_destroy", "qsim_set_ising", "q
            "qsim_apply_qaoa", "qsim_apply_aqa", "qsim_aqa_angles", "qsim_expect_hc", "qsim_norm2",
            "qsim_success_prob", "qsim_get_amplitudes", "qsim_energies", "qsim_sync",
            "qsim_plan_counts", "qsim_plan_positions", "qsim_nccl_unique_id",
-           "qsim_profile_enable", "qsim_profile_read", "qsim_kernel_launches", "qsim_last_error",
+           "qsim_bench_pass", "qsim_profile_enable", "qsim_profile_read", "qsim_kernel_launches", "qsim_last_error",
            "qsim_version"]
 
 
@@ -75,6 +75,7 @@ lib.qsim_plan_counts.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctype
                                  ctypes.POINTER(ctypes.c_int), _U64]
 lib.qsim_plan_positions.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
 lib.qsim_nccl_unique_id.argtypes = [ctypes.c_void_p]
+lib.qsim_bench_pass.argtypes = [_H, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D]
 lib.qsim_profile_enable.argtypes = [_H, ctypes.c_int]
 lib.qsim_profile_read.argtypes = [_H, _D, _U64, _D]
 lib.qsim_kernel_launches.argtypes = [_H]
@@ -204,6 +205,12 @@ def qsim_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib.qsim_nccl_unique_id(buf))
     return buf.raw
+
+
+def qsim_bench_pass(h, set_index: int, phase: bool, reps: int = 5) -> float:
+    out = ctypes.c_double()
+    _check(lib.qsim_bench_pass(h, int(set_index), int(bool(phase)), int(reps), ctypes.byref(out)), h)
+    return out.value
 
 
 def qsim_profile_enable(h, on: bool = True) -> None:

@@ -1,0 +1,29 @@
+"""Time each tile-set pass type in isolation: python tools/passbench.py --n 30"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, nargs="+", default=[30])
+ap.add_argument("--reps", type=int, default=5)
+a = ap.parse_args()
+torch.cuda.set_device(0)
+from paper_2104_03293_b200 import instances as inst  # noqa: E402
+from paper_2104_03293_b200 import qsim as Q  # noqa: E402
+
+for n in a.n:
+    h, J = inst.random_ising(n, 1)
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        nsets = 1 + -(-(n - 12) // 9)
+        ideal = 32 * 2.0 ** n / 6455.9e9 * 1e3
+        for k in range(nsets):
+            for ph in (0, 1):
+                ms = Q.qsim_bench_pass(s.h, k, ph, a.reps)
+                print(f"n={n} set={k} phase={ph} {ms:.3f} ms  ({ideal / ms * 100:.1f}% of measured HBM peak)",
+                      flush=True)
