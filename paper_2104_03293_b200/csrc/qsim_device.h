@@ -5,6 +5,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+struct CUtensorMap_st;  // <cuda.h>
+
 namespace qk {
 
 typedef unsigned long long u64;
@@ -51,6 +53,8 @@ struct PassParams {
     double *part;        // reduce partials, 2 per CTA
     const void *rec;     // per-tile records (TileRec), written by tile_fields_kernel
     int prefetch;        // L2-prefetch the CTA's next tile
+    int tm_clen[5];      // TMA path: tile id bits feeding each tensor-map coordinate (0: tile dim)
+    int tm_cshift[5];
 };
 
 constexpr size_t TILE_REC_BYTES = 320;  // sizeof(TileRec)
@@ -80,6 +84,10 @@ struct ProbeSet {
 };
 
 size_t pass_smem_bytes();
+size_t tma_smem_bytes();
+cudaError_t setup_tma_kernels();
+// TMA-pipelined pass (qsim_tma.cu); `tensor_map` points to a CUtensorMap (128 B)
+cudaError_t launch_tma_pass(const ::CUtensorMap_st &tensor_map, const PassParams &P, int grid, cudaStream_t s);
 cudaError_t setup_kernels();
 cudaError_t launch_pass(const PassParams &P, int grid, cudaStream_t s);
 cudaError_t launch_tile_fields(const PassParams &P, void *rec, cudaStream_t s);

@@ -7,6 +7,8 @@
 //  * angle generation for AQA (eq:beta_k / eq:gamma_k),
 //  * permutation bookkeeping (the paper's "local permutation array"),
 //  * NCCL all-to-all qubit swap and all-reduce of the reduction scalars.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -33,6 +35,12 @@ struct TileSet {
     u64 lmask;
     unsigned own;  // tile-bit mask of the bits this set mixes
     bool full12;   // the 12-bit set of bits 0..11 (all mixed) vs a "run" set with passengers
+    // TMA view of the shard for this set (units: doubles): up to 5 dims, innermost first
+    int tm_rank;
+    cuuint64_t tm_dim[5], tm_stride[5];  // stride in bytes of dims 1..rank-1
+    cuuint32_t tm_box[5];
+    int tm_clen[5], tm_cshift[5];        // tile id bits feeding non-tile coordinates
+    bool tm_ok;
     int nseg;
     int seg_len[8], seg_dst[8];
     u64 ntiles;
@@ -66,6 +74,48 @@ TileSet make_set(int m, const std::vector<int> &Lpos, unsigned own) {
     }
     S.nseg = ns;
     S.ntiles = 1ull << (m - qk::KT);
+    // ---- TMA tensor view: walk the bits [0, m) as maximal tile / non-tile segments.  Tile
+    // segments become box dims (<= 8 bits, box <= 256; the innermost carries re/im, so <= 7
+    // bits), non-tile segments become single-coordinate dims fed by tile-id bits in ascending
+    // order (matching tile_base).
+    S.tm_rank = 0;
+    S.tm_ok = true;
+    int ubit = 0;
+    int b = 0;
+    while (b < m && S.tm_ok) {
+        const bool tile = (lm >> b) & 1ull;
+        int e = b;
+        while (e < m && (((lm >> e) & 1ull) != 0) == tile) ++e;
+        int len = e - b;
+        int pos = b;
+        while (len > 0) {
+            if (S.tm_rank == 5) { S.tm_ok = false; break; }
+            const int d = S.tm_rank;
+            int take;
+            if (tile) take = std::min(len, d == 0 ? 7 : 8);
+            else take = len;
+            const cuuint64_t sz = 1ull << take;
+            S.tm_dim[d] = (d == 0) ? 2 * sz : sz;
+            S.tm_stride[d] = 16ull << pos;
+            S.tm_box[d] = tile ? (cuuint32_t)S.tm_dim[d] : 1u;
+            S.tm_clen[d] = tile ? 0 : take;
+            S.tm_cshift[d] = tile ? 0 : ubit;
+            if (!tile) ubit += take;
+            if (d == 0 && !tile) S.tm_ok = false;  // bit 0 is always a tile bit
+            pos += take;
+            len -= take;
+            ++S.tm_rank;
+        }
+        b = e;
+    }
+    // pad to 5 dims (the kernel always issues the .5d form of cp.async.bulk.tensor)
+    for (int d = S.tm_rank; d < 5; ++d) {
+        S.tm_dim[d] = 1;
+        S.tm_stride[d] = 16ull << m;  // past the end of the shard; dim size 1
+        S.tm_box[d] = 1;
+        S.tm_clen[d] = 0;
+        S.tm_cshift[d] = 0;
+    }
     return S;
 }
 
@@ -204,6 +254,7 @@ struct qsim {
     bool res_valid = false;
     uint64_t launches = 0;
     int prefetch = 1;          // L2 prefetch of the next tile (QSIM_PREFETCH=0 disables, for experiments)
+    int use_tma = 1;           // TMA-pipelined pass kernel (QSIM_KERNEL=v4 selects the register-direct one)
     std::string err;
     // optional per-pass timing (CUDA events on the handle's stream around each pass launch)
     bool prof = false;
@@ -291,6 +342,45 @@ qk::PassParams base_params(qsim *q, const TileSet &S) {
     // every tile touches up to 512 distinct 2 MiB pages and prefetching slows them (measured)
     P.prefetch = q->prefetch && S.full12;
     return P;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult qr;
+        void *ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qr) == cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+// launch one pass: TMA-pipelined kernel (one CTA per SM) or the register-direct kernel
+int launch_pass_any(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out) {
+    if (q->use_tma) {
+        auto enc = tmap_encoder();
+        if (!enc) return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        CUtensorMap tm;
+        cuuint32_t es[5] = {1, 1, 1, 1, 1};
+        CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5u, (void *)q->psi, S.tm_dim,
+                         S.tm_stride + 1, S.tm_box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+        for (int d = 0; d < 5; ++d) {
+            P.tm_clen[d] = S.tm_clen[d];
+            P.tm_cshift[d] = S.tm_cshift[d];
+        }
+        int grid = (int)std::min<u64>((u64)q->num_sms, S.ntiles);
+        CK(qk::launch_tma_pass(tm, P, grid, q->st));
+        *grid_out = grid;
+    } else {
+        int grid = grid_for(q, S.ntiles);
+        CK(qk::launch_pass(P, grid, q->st));
+        *grid_out = grid;
+    }
+    q->launches++;
+    return QSIM_OK;
 }
 
 int finish_reduce(qsim *q, int nparts) {
@@ -448,15 +538,17 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
             CK(qk::launch_tile_fields(P, q->d_rec, q->st));
             q->launches++;
         }
-        int grid = grid_for(q, S.ntiles);
+        int grid = 0;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (q->prof) {
             int rc = prof_events(q, &e0, &e1);
             if (rc) return rc;
             CK(cudaEventRecord(e0, q->st));
         }
-        CK(qk::launch_pass(P, grid, q->st));
-        q->launches++;
+        {
+            int rc = launch_pass_any(q, S, P, &grid);
+            if (rc) return rc;
+        }
         if (q->prof) {
             CK(cudaEventRecord(e1, q->st));
             // algorithmic HBM bytes: read + write of the shard, write only for the init pass
@@ -611,6 +703,12 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     }
     q->pending_plus = true;
     if (const char *e = std::getenv("QSIM_PREFETCH")) q->prefetch = std::atoi(e);
+    if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
+    if (q->use_tma) {
+        CK(qk::setup_tma_kernels());
+        for (const TileSet &S : q->sets)
+            if (!S.tm_ok) q->use_tma = 0;
+    }
     return QSIM_OK;
 }
 
@@ -852,8 +950,9 @@ int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
     std::complex<double> k1, k2;
     P.c1 = mix_coef(0.3, k1);
     P.c2 = mix_coef(-0.2, k2);
-    P.mix1 = S.own;
-    P.mix2 = phase ? S.own : 0u;
+    P.mix1 = phase < 0 ? 0u : S.own;  // phase < 0: copy only (memory-pattern probe)
+    P.mix2 = phase > 0 ? S.own : 0u;
+    if (phase < 0) phase = 0;
     std::complex<double> sc = cpow_int(k1, __builtin_popcount(P.mix1)) * cpow_int(k2, __builtin_popcount(P.mix2));
     P.scale = make_double2(sc.real(), sc.imag());
     P.kind = S.full12 ? (phase ? qk::K_TURN12 : qk::K_PLAIN12) : (phase ? qk::K_TURN_RUN : qk::K_PLAIN_RUN);
@@ -865,10 +964,14 @@ int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    int grid = grid_for(q, S.ntiles);
-    CK(qk::launch_pass(P, grid, q->st));  // warm-up
+    int grid = 0;
+    rc = launch_pass_any(q, S, P, &grid);  // warm-up
+    if (rc) return rc;
     CK(cudaEventRecord(e0, q->st));
-    for (int r = 0; r < reps; ++r) CK(qk::launch_pass(P, grid, q->st));
+    for (int r = 0; r < reps; ++r) {
+        rc = launch_pass_any(q, S, P, &grid);
+        if (rc) return rc;
+    }
     CK(cudaEventRecord(e1, q->st));
     CK(cudaEventSynchronize(e1));
     float ms = 0.f;

@@ -75,7 +75,7 @@ __device__ __forceinline__ double eh_term(const double *hp, const double *Jp, in
 }
 
 // E(X) for one full physical index X, composed from the same pieces (probe kernel).
-__device__ double energy_point(const double *hp, const double *Jp, int n, const int *L, int k,
+__device__ inline double energy_point(const double *hp, const double *Jp, int n, const int *L, int k,
                                u64 lmask, u64 X) {
     double e = 0.0;
     for (int j = 0; j < n; ++j)
@@ -210,7 +210,7 @@ struct ThreadEnergy {
 };
 
 template <int F>
-__device__ ThreadEnergy thread_energy(const double *Jp, int n, const int *L, int lane, int warp, int ft) {
+__device__ inline ThreadEnergy thread_energy(const double *Jp, int n, const int *L, int lane, int warp, int ft) {
     const int t = Frame<F>::tthr(lane, warp) ^ ft;  // spins of the flipped index
     const unsigned rmask = 0x1Fu << Frame<F>::RB;
     ThreadEnergy te;
@@ -240,7 +240,7 @@ __device__ ThreadEnergy thread_energy(const double *Jp, int n, const int *L, int
 // E_RR(j) = sum_{r<r'} J_{R_r R_r'} s_r(j) s_r'(j) for the 32 register patterns
 // (j already xor-ed with the register-bit flips by the caller)
 template <int F>
-__device__ double err_of(const double *Jp, int n, const int *L, int j) {
+__device__ inline double err_of(const double *Jp, int n, const int *L, int j) {
     double e = 0.0;
     for (int r = 0; r < 5; ++r)
         for (int r2 = r + 1; r2 < 5; ++r2)
@@ -264,8 +264,6 @@ struct __align__(16) TileRec {
     double pad;
 };
 
-__device__ __forceinline__ double2 ldg2(const double2 *p) { return __ldg(p); }
-
 // psi_z *= e^{-i gamma E} for the thread's 32 amplitudes (frame F):
 //   E = E_H + sum_{i in T} s_i h'_i + E_TT + sum_r s_r (h'_{R_r} + w_r) + E_RR(j)
 // pconst = kappa-scale * e^{-i gamma E_TT};  u[r] = e^{-i gamma w_r}.
@@ -274,18 +272,18 @@ __device__ __forceinline__ double2 ldg2(const double2 *p) { return __ldg(p); }
 template <int F>
 __device__ __forceinline__ void apply_phase(double2 (&v)[NR], const TileRec *R, int tthr, int fr, double2 pconst,
                                             const double2 (&u)[5], const double2 *PRR) {
-    double2 base = cmul(ldg2(&R->f[12]), pconst);
+    double2 base = cmul(R->f[12], pconst);
 #pragma unroll
     for (int i = 0; i < KT; ++i) {
         if (i >= Frame<F>::RB && i < Frame<F>::RB + 5) continue;
-        const double2 fi = ldg2(&R->f[i]);
+        const double2 fi = R->f[i];
         const double sg = ((tthr >> i) & 1) ? 1.0 : -1.0;
         base = cmul(base, make_double2(fi.x, sg * fi.y));
     }
     double2 g[5];
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
-        const double2 gr = cmul(ldg2(&R->f[Frame<F>::RB + r]), u[r]);
+        const double2 gr = cmul(R->f[Frame<F>::RB + r], u[r]);
         g[r] = ((fr >> r) & 1) ? conjd(gr) : gr;  // flipped register bit: s_r -> -s_r
     }
     // lo over register bits 0,1 (times base): {c(A), B, c(B), A} with A = g0 g1, B = g0 c(g1)
@@ -316,17 +314,17 @@ __device__ __forceinline__ void accumulate(const double2 (&v)[NR], const TileRec
                                            const ThreadEnergy &te, const double *eRR, double &acc_e,
                                            double &acc_n) {
     double Q[NR];
-    double eb = __ldg(&R->e[12]) + te.eTT;
+    double eb = R->e[12] + te.eTT;
 #pragma unroll
     for (int i = 0; i < KT; ++i) {
         if (i >= Frame<F>::RB && i < Frame<F>::RB + 5) continue;
-        const double ei = __ldg(&R->e[i]);
+        const double ei = R->e[i];
         eb += ((tthr >> i) & 1) ? ei : -ei;
     }
     Q[0] = eb;
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
-        const double a0 = __ldg(&R->e[Frame<F>::RB + r]) + te.w[r];
+        const double a0 = R->e[Frame<F>::RB + r] + te.w[r];
         const double a = ((fr >> r) & 1) ? -a0 : a0;
 #pragma unroll
         for (int j = 0; j < (1 << r); ++j) {

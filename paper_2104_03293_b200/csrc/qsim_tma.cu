@@ -1,0 +1,325 @@
+// qsim_tma.cu -- TMA-pipelined tile pass (sm_100a), the streaming hot loop of SURVEY §8a
+// rows a3-a7.
+//
+// One persistent CTA per SM: NG consumer groups of 128 threads (4 warps, 32 amplitudes per
+// thread) and a ring of 3 shared-memory stages of one 2^12-amplitude tile (64 KiB) each.
+// Tile i of the CTA lives in stage i % 3 and is processed by group i % NG.  A tile and its
+// per-tile energy record arrive together by TMA (cp.async.bulk.tensor 5-D box + a 320 B bulk
+// copy) on the stage's mbarrier.  The group then runs the pass program of qsim_kernels.cuh:
+// each round reads the tile from the stage in one register frame, applies butterflies (and
+// the phase), and writes it back; the frame of the last round is read, the stage is released
+// at once (the group's elected thread issues the TMA of tile i+3 into it) and the tile is
+// finished in registers and stored to HBM with coalesced 16-byte stores.  Shared memory is
+// linear (element t at 16 t); frame Y is lane-skewed instead, so every frame is
+// bank-conflict free.
+#include <cuda.h>
+
+#include "qsim_device.h"
+#include "qsim_kernels.cuh"
+
+namespace qk {
+
+constexpr int NSTAGE = 3;
+constexpr int TMA_NG = 2;  // consumer groups per CTA
+
+struct TmaSmem {
+    static constexpr size_t stage = SM_TILE_BYTES;
+    static constexpr size_t rec_off = NSTAGE * stage;
+    static constexpr size_t bar_off = rec_off + NSTAGE * TILE_REC_BYTES;
+    static constexpr size_t iss_off = bar_off + 32;  // int issued[NSTAGE]
+    static constexpr size_t cs_off = bar_off + 64;
+    static constexpr size_t red_off = cs_off + ((sizeof(CtaShared) + 15) / 16) * 16;
+    static constexpr size_t total = red_off + 2 * 8 * TMA_NG * 4;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *tm, const int (&c)[5], uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void group_bar(int g) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(128) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// linear-layout frame I/O; frame Y skews its low register bits by the lane so that every
+// quarter-warp hits 8 different 16-byte bank groups
+template <int F>
+__device__ __forceinline__ void lds_frame(double2 (&v)[NR], const double2 *sm, int lane, int warp) {
+    const int t = Frame<F>::tthr(lane, warp);
+    const int sk = (F == FY) ? (lane & 7) : 0;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) v[j] = sm[t | ((j ^ sk) << Frame<F>::RB)];
+}
+template <int F>
+__device__ __forceinline__ void sts_frame(const double2 (&v)[NR], double2 *sm, int lane, int warp) {
+    const int t = Frame<F>::tthr(lane, warp);
+    const int sk = (F == FY) ? (lane & 7) : 0;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) sm[t | ((j ^ sk) << Frame<F>::RB)] = v[j];
+}
+
+struct TmaIssue {
+    const CUtensorMap *tm;
+    const TileRec *grec;
+    double2 *stages;
+    TileRec *srec;
+    uint64_t *full;
+    volatile int *issued;  // tiles issued into each stage so far
+};
+
+__device__ __forceinline__ void issue_tile(const PassParams &P, const TmaIssue &I, u64 ut, int s, bool load_state,
+                                           bool load_rec) {
+    const uint32_t bytes = (load_state ? (uint32_t)SM_TILE_BYTES : 0u) + (load_rec ? (uint32_t)TILE_REC_BYTES : 0u);
+    if (!bytes) {
+        I.issued[s] = I.issued[s] + 1;
+        return;
+    }
+    mbar_expect_tx(&I.full[s], bytes);
+    if (load_state) {
+        int c[5];
+#pragma unroll
+        for (int d = 0; d < 5; ++d)
+            c[d] = P.tm_clen[d] ? (int)((ut >> P.tm_cshift[d]) & ((1ull << P.tm_clen[d]) - 1ull)) : 0;
+        tma_load_5d(I.stages + (size_t)s * TILE, I.tm, c, &I.full[s]);
+    }
+    if (load_rec) bulk_load(I.srec + s, I.grec + ut, (uint32_t)TILE_REC_BYTES, &I.full[s]);
+    __threadfence_block();
+    I.issued[s] = I.issued[s] + 1;
+}
+
+// Stage s is consumed alternately by the two groups, so a group may reach its wait for tile i
+// while the stage still holds tile i-3 (not yet consumed by the other group).  The parity wait
+// would then test the *preceding* phase and pass at once; waiting first until tile i has been
+// issued into the stage (which happens only after tile i-3 was consumed) makes it exact.
+__device__ __forceinline__ void wait_tile(const TmaIssue &I, u64 i) {
+    const int s = (int)(i % NSTAGE);
+    const int need = (int)(i / NSTAGE) + 1;
+    while (I.issued[s] < need) __nanosleep(32);
+    mbar_wait(&I.full[s], (uint32_t)((i / NSTAGE) & 1));
+}
+
+constexpr unsigned TMX = 0xF80u, TMY = 0x01Fu, TMZ = 0x060u, TMW = 0x078u;
+
+template <int KIND>
+__global__ void __launch_bounds__(TMA_NG * 128, 1)
+    tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    double2 *stages = reinterpret_cast<double2 *>(smem);
+    TileRec *srec = reinterpret_cast<TileRec *>(smem + TmaSmem::rec_off);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + TmaSmem::bar_off);
+    CtaShared &cs = *reinterpret_cast<CtaShared *>(smem + TmaSmem::cs_off);
+    double *red = reinterpret_cast<double *>(smem + TmaSmem::red_off);
+    constexpr bool RUN = (KIND == K_PLAIN_RUN || KIND == K_TURN_RUN);
+    constexpr bool TURN = (KIND == K_TURN12 || KIND == K_TURN_RUN);
+    constexpr int FE = RUN ? FW : FZ;
+
+    const int tid = threadIdx.x, g = tid >> 7, gt = tid & 127, lane = gt & 31, warp = gt >> 5;
+    const int n = P.n;
+    const bool need_e = TURN || P.reduce;
+    const bool load_state = !(TURN && P.init);
+    const u64 ntl = (P.ntiles > blockIdx.x) ? (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    volatile int *issued = reinterpret_cast<volatile int *>(smem + TmaSmem::iss_off);
+    const TmaIssue I{&tmap, reinterpret_cast<const TileRec *>(P.rec), stages, srec, full, issued};
+
+    if (tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) {
+            mbar_init(&full[s], 1);
+            issued[s] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int i = 0; i < NSTAGE && (u64)i < ntl; ++i)
+            issue_tile(P, I, blockIdx.x + (u64)i * gridDim.x, i, load_state, need_e);
+
+    int ft = 0;  // tile-bit flips (X gates of the |tan beta| > 1 mixer form)
+#pragma unroll
+    for (int i = 0; i < KT; ++i) ft |= (int)((P.flip >> P.L[i]) & 1ull) << i;
+    const int tE = Frame<FE>::tthr(lane, warp) ^ ft;
+    const int fr = (ft >> Frame<FE>::RB) & 0x1F;
+
+    ThreadEnergy te;
+    double2 pconst = P.scale;
+    double2 u[5];
+    te.eTT = 0.0;
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+        te.w[r] = 0.0;
+        u[r] = make_double2(1.0, 0.0);
+    }
+    if (need_e) {
+        te = thread_energy<FE>(P.Jp, n, P.L, lane, warp, ft);
+        if (TURN) {
+            pconst = cmul(P.scale, expmi(P.gamma * te.eTT));
+#pragma unroll
+            for (int r = 0; r < 5; ++r) u[r] = expmi(P.gamma * te.w[r]);
+        }
+        if (tid < NR) {
+            const double e = err_of<FE>(P.Jp, n, P.L, tid ^ fr);
+            cs.eRR[tid] = e;
+            cs.PRR[tid] = TURN ? expmi(P.gamma * e) : make_double2(1.0, 0.0);
+        }
+    }
+    const u64 offX = thread_offset<FX>(P.L, lane, warp);
+    const u64 offS = thread_offset<RUN ? FW : FZ>(P.L, lane, warp);
+    __syncthreads();
+
+    double acc_e = 0.0, acc_n = 0.0;
+    double2 v[NR];
+    for (u64 i = g; i < ntl; i += TMA_NG) {
+        const int s = (int)(i % NSTAGE);
+        const u64 ut = blockIdx.x + i * gridDim.x;
+        const u64 tb = tile_base(P, ut);
+        double2 *sm = stages + (size_t)s * TILE;
+        const TileRec *R = srec + s;
+        if (load_state || need_e) wait_tile(I, i);
+        // ------------------------------------------------ rounds up to the last smem read
+        if (load_state) {
+            lds_frame<FX>(v, sm, lane, warp);
+            mix_frame<FX>(v, P.mix1 & TMX, P.c1.t);
+            sts_frame<FX>(v, sm, lane, warp);
+            group_bar(g);
+            if (RUN) {
+                lds_frame<FW>(v, sm, lane, warp);
+                if (TURN) mix_frame<FW>(v, P.mix1 & TMW, P.c1.t);
+            } else {
+                lds_frame<FY>(v, sm, lane, warp);
+                mix_frame<FY>(v, P.mix1 & TMY, P.c1.t);
+                sts_frame<FY>(v, sm, lane, warp);
+                group_bar(g);
+                lds_frame<FZ>(v, sm, lane, warp);
+                if (TURN) mix_frame<FZ>(v, P.mix1 & TMZ, P.c1.t);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < NR; ++j) v[j] = make_double2(P.a0, 0.0);
+        }
+        if (TURN) {
+            apply_phase<FE>(v, R, tE, fr, pconst, u, cs.PRR);
+            if (RUN) {
+                mix_frame<FW>(v, P.mix2 & TMW, P.c2.t);
+                sts_frame<FW>(v, sm, lane, warp);
+                group_bar(g);
+            } else {
+                mix_frame<FZ>(v, P.mix2 & TMZ, P.c2.t);
+                sts_frame<FZ>(v, sm, lane, warp);
+                group_bar(g);
+                lds_frame<FY>(v, sm, lane, warp);
+                mix_frame<FY>(v, P.mix2 & TMY, P.c2.t);
+                sts_frame<FY>(v, sm, lane, warp);
+                group_bar(g);
+            }
+            lds_frame<FX>(v, sm, lane, warp);
+        }
+        // ------------------------------------------------ release the stage, refill it
+        // (a reducing pass reads the stage's tile record, so it finishes before the refill)
+        const bool late_release = !TURN && P.reduce;
+        if (!late_release) {
+            fence_async_smem();
+            group_bar(g);
+            if (gt == 0 && i + NSTAGE < ntl)
+                issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+        }
+        // ------------------------------------------------ finish in registers, store
+        if (TURN) {
+            mix_frame<FX>(v, P.mix2 & TMX, P.c2.t);
+            store_tile<FX>(v, P.psi + tb + offX, P.L);
+        } else {
+            if (RUN) mix_frame<FW>(v, P.mix1 & TMW, P.c1.t);
+            else mix_frame<FZ>(v, P.mix1 & TMZ, P.c1.t);
+            if (P.scale.x != 1.0 || P.scale.y != 0.0) {
+#pragma unroll
+                for (int j = 0; j < NR; ++j) v[j] = cmul(v[j], P.scale);
+            }
+            if (P.reduce) accumulate<FE>(v, R, tE, fr, te, cs.eRR, acc_e, acc_n);
+            if (late_release) {
+                fence_async_smem();
+                group_bar(g);
+                if (gt == 0 && i + NSTAGE < ntl)
+                    issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+            }
+            store_tile<RUN ? FW : FZ>(v, P.psi + tb + offS, P.L);
+        }
+    }
+    if (P.reduce) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            acc_e += __shfl_xor_sync(0xffffffffu, acc_e, o);
+            acc_n += __shfl_xor_sync(0xffffffffu, acc_n, o);
+        }
+        const int w = tid >> 5;
+        if (lane == 0) {
+            red[2 * w] = acc_e;
+            red[2 * w + 1] = acc_n;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double a = 0.0, b = 0.0;
+            for (int k = 0; k < TMA_NG * 4; ++k) {
+                a += red[2 * k];
+                b += red[2 * k + 1];
+            }
+            P.part[2 * blockIdx.x] = a;
+            P.part[2 * blockIdx.x + 1] = b;
+        }
+    }
+}
+
+size_t tma_smem_bytes() { return TmaSmem::total; }
+
+cudaError_t setup_tma_kernels() {
+    cudaError_t e;
+    e = cudaFuncSetAttribute(tma_pass_kernel<K_PLAIN12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(tma_pass_kernel<K_PLAIN_RUN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(tma_pass_kernel<K_TURN12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(tma_pass_kernel<K_TURN_RUN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
+}
+
+cudaError_t launch_tma_pass(const CUtensorMap &tm, const PassParams &P, int grid, cudaStream_t s) {
+    const size_t sh = TmaSmem::total;
+    switch (P.kind) {
+        case K_PLAIN12: tma_pass_kernel<K_PLAIN12><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
+        case K_PLAIN_RUN: tma_pass_kernel<K_PLAIN_RUN><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
+        case K_TURN12: tma_pass_kernel<K_TURN12><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
+        case K_TURN_RUN: tma_pass_kernel<K_TURN_RUN><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace qk

@@ -207,9 +207,9 @@ def qsim_nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def qsim_bench_pass(h, set_index: int, phase: bool, reps: int = 5) -> float:
+def qsim_bench_pass(h, set_index: int, phase: int, reps: int = 5) -> float:
     out = ctypes.c_double()
-    _check(lib.qsim_bench_pass(h, int(set_index), int(bool(phase)), int(reps), ctypes.byref(out)), h)
+    _check(lib.qsim_bench_pass(h, int(set_index), int(phase), int(reps), ctypes.byref(out)), h)
     return out.value
 
 

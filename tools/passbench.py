@@ -23,7 +23,7 @@ for n in a.n:
         nsets = 1 + -(-(n - 12) // 9)
         ideal = 32 * 2.0 ** n / 6455.9e9 * 1e3
         for k in range(nsets):
-            for ph in (0, 1):
+            for ph in (-1, 0, 1):
                 ms = Q.qsim_bench_pass(s.h, k, ph, a.reps)
                 print(f"n={n} set={k} phase={ph} {ms:.3f} ms  ({ideal / ms * 100:.1f}% of measured HBM peak)",
                       flush=True)
