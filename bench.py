@@ -285,7 +285,7 @@ def main():
             "sec_per_layer": ms_step / 1e3 / p,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "qk::pass_kernel", "avg_launch_ms": avg_pass_ms,
+                         "kernel": "qk::tma_pass_kernel", "avg_launch_ms": avg_pass_ms,
                          "launches": pass_cnt, "alg_bytes_per_launch": avg_bytes,
                          "pass_share_of_step": pass_ms_max / ms_max},
             "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")} if cpu else None),

@@ -66,8 +66,9 @@ int qsim_create(int n, int precision, qsim_t **out);
 /* Multi-GPU / embedding variant.  The state is partitioned over `world` = 2^g ranks
  * on its top g physical qubits (the "global" qubits): rank r holds the
  * 2^(n-g) amplitudes whose global bits equal r.  `nccl_unique_id` points to the 128
- * bytes of an ncclUniqueId created on rank 0 and broadcast to all ranks (ignored
- * when world == 1).  `state_buf` (device pointer, optional) provides caller-owned
+ * bytes of an ncclUniqueId created on rank 0 (qsim_nccl_unique_id) and broadcast to all
+ * ranks; an id initialises exactly one communicator, so use a fresh id per handle
+ * (ignored when world == 1).  `state_buf` (device pointer, optional) provides caller-owned
  * storage of buf_bytes >= 16 * 2^(n-g) bytes (the library then does not allocate
  * the state); `cuda_stream` (cudaStream_t, optional) is the stream all work is
  * enqueued on.  world must be a power of two <= 8 with n - g >= 13. */
