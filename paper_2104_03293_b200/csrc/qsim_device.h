@@ -55,6 +55,10 @@ struct PassParams {
     int prefetch;        // L2-prefetch the CTA's next tile
     int tm_clen[5];      // TMA path: tile id bits feeding each tensor-map coordinate (0: tile dim)
     int tm_cshift[5];
+    // fused global-qubit swap: amplitude at local x = (c | y), c = top g bits, is stored at
+    // dst[c][(rank << (m-g)) | y] (dst[c] = rank c's other state buffer, mapped over NVLink)
+    int swap_store, gbits, rank;
+    double2 *dst[8];
 };
 
 constexpr size_t TILE_REC_BYTES = 320;  // sizeof(TileRec)

@@ -51,7 +51,8 @@ struct PassOp {
     bool init, phase, reduce;
     unsigned mix1, mix2;
     double b1, b2, gamma;
-    bool swap_after;  // multi-GPU: global-qubit swap after this pass
+    bool swap_after;  // multi-GPU: global-qubit swap (NCCL, in place) after this pass
+    bool swap_fused;  // multi-GPU: this pass stores its output swapped into the peers' buffers
 };
 
 TileSet make_set(int m, const std::vector<int> &Lpos, unsigned own) {
@@ -155,7 +156,7 @@ std::vector<TileSet> build_sets(int m) {
 // with beta_{k-1}, phase_k, set with beta_k), the other sets, then the swap of the top
 // g local bits with the global bits: P p + 1 passes, p swaps.
 std::vector<PassOp> build_schedule(int nsets, int g, int p, const double *gam, const double *bet,
-                                   bool first_init) {
+                                   bool first_init, bool fused = false) {
     std::vector<PassOp> ops;
     const int P = nsets;
     if (g == 0) {
@@ -164,28 +165,35 @@ std::vector<PassOp> build_schedule(int nsets, int g, int p, const double *gam, c
         if (P > 1) order.push_back(0);
         for (int i = 2; i < P; ++i) order.push_back(i);
         auto seq = [&](int k, int idx) { return order[(k % 2 == 0) ? idx : P - 1 - idx]; };
-        ops.push_back({seq(0, 0), first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false});
+        ops.push_back({seq(0, 0), first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false, false});
         for (int k = 0; k < p; ++k) {
             for (int idx = 1; idx < P; ++idx) {
                 int s = seq(k, idx);
                 if (idx == P - 1 && k < p - 1)
-                    ops.push_back({s, false, true, false, ~0u, ~0u, bet[k], bet[k + 1], gam[k + 1], false});
+                    ops.push_back({s, false, true, false, ~0u, ~0u, bet[k], bet[k + 1], gam[k + 1], false, false});
                 else
-                    ops.push_back({s, false, false, false, ~0u, 0u, bet[k], 0.0, 0.0, false});
+                    ops.push_back({s, false, false, false, ~0u, 0u, bet[k], 0.0, 0.0, false, false});
             }
         }
     } else {
+        // G > 1: per layer the boundary pass on the top run (arrivals of the last swap get
+        // beta_{k-1}, phase_k, the set gets beta_k), then the other sets with beta_k.  The swap
+        // of the top g local bits with the global bits either rides on the boundary pass's
+        // stores (fused: output written straight into the peers' second buffers over NVLink)
+        // or follows the layer's last pass (NCCL, in place).  The trailing pass gives the last
+        // arrivals beta_{p-1}.
         const int top = P - 1;
         const unsigned arrivals = ((1u << g) - 1) << (qk::KT - g);  // top g tile bits of the top set
-        ops.push_back({top, first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false});
         for (int k = 0; k < p; ++k) {
-            for (int s = P - 2; s >= 0; --s) ops.push_back({s, false, false, false, ~0u, 0u, bet[k], 0.0, 0.0, false});
-            ops.back().swap_after = true;
-            if (k < p - 1)
-                ops.push_back({top, false, true, false, arrivals, ~0u, bet[k], bet[k + 1], gam[k + 1], false});
+            if (k == 0)
+                ops.push_back({top, first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false, fused});
             else
-                ops.push_back({top, false, false, false, arrivals, 0u, bet[k], 0.0, 0.0, false});
+                ops.push_back({top, false, true, false, arrivals, ~0u, bet[k - 1], bet[k], gam[k], false, fused});
+            for (int s = P - 2; s >= 0; --s)
+                ops.push_back({s, false, false, false, ~0u, 0u, bet[k], 0.0, 0.0, false, false});
+            if (!fused) ops.back().swap_after = true;
         }
+        ops.push_back({top, false, false, false, arrivals, 0u, bet[p - 1], 0.0, 0.0, false, false});
     }
     ops.back().reduce = true;
     return ops;
@@ -236,6 +244,12 @@ struct qsim {
     bool own_psi = false;
     double2 *tmp = nullptr;  // swap buffer (multi-GPU, when memory allows)
     void *user_buf = nullptr; // caller-owned state storage (never freed here)
+    // fused swap: both state buffers of every rank mapped through CUDA IPC
+    bool fused_swap = false;
+    int cur = 0;                       // which of bufs[] currently holds the state
+    double2 *bufs[2] = {nullptr, nullptr};
+    double2 *peer[2][8] = {};          // peer[b][c] = rank c's buffer b (own buffer for c == rank)
+    double *d_bar = nullptr;           // 1-double scratch for the NCCL barrier
     cudaStream_t st = nullptr;
     bool own_stream = false;
     ncclComm_t comm = nullptr;
@@ -391,15 +405,31 @@ int finish_reduce(qsim *q, int nparts) {
     return QSIM_OK;
 }
 
+// bookkeeping of a swap of positions [m-g, m) <-> [m, n): permutation parity and the flip
+// mask (its bits travel with the qubits)
+void swap_bookkeeping(qsim *q) {
+    const u64 gm = (1ull << q->g) - 1ull;
+    const u64 lo = (q->flip >> (q->m - q->g)) & gm, hi = (q->flip >> q->m) & gm;
+    q->flip &= ~((gm << (q->m - q->g)) | (gm << q->m));
+    q->flip |= (hi << (q->m - q->g)) | (lo << q->m);
+    q->parity ^= 1;
+}
+
+// after a fused swap pass: wait until every rank's pass (and its NVLink stores) is done, then
+// the other buffer holds the state
+int finish_fused_swap(qsim *q) {
+    NK(ncclAllReduce(q->d_bar, q->d_bar, 1, ncclDouble, ncclSum, q->comm, q->st));
+    q->cur ^= 1;
+    q->psi = q->bufs[q->cur];
+    q->tmp = q->bufs[q->cur ^ 1];
+    swap_bookkeeping(q);
+    return QSIM_OK;
+}
+
 // global-qubit swap: positions [m-g, m) <-> [m, n); rank r's chunk c <-> rank c's chunk r
 int do_swap(qsim *q) {
     const int G = q->world;
-    {   // the flip mask travels with the qubits: positions [m-g, m) <-> [m, n)
-        const u64 gm = (1ull << q->g) - 1ull;
-        const u64 lo = (q->flip >> (q->m - q->g)) & gm, hi = (q->flip >> q->m) & gm;
-        q->flip &= ~((gm << (q->m - q->g)) | (gm << q->m));
-        q->flip |= (hi << (q->m - q->g)) | (lo << q->m);
-    }
+    swap_bookkeeping(q);
     const u64 chunk = 1ull << (q->m - q->g);  // amplitudes per chunk
     const size_t cbytes = chunk * sizeof(double2);
     if (q->tmp) {
@@ -413,6 +443,7 @@ int do_swap(qsim *q) {
         CK(cudaMemcpyAsync(q->tmp + q->rank * chunk, q->psi + q->rank * chunk, cbytes,
                            cudaMemcpyDeviceToDevice, q->st));
         std::swap(q->psi, q->tmp);
+        if (q->fused_swap) q->cur ^= 1;
     } else {
         // in place through a bounded staging ring: piece by piece, copy the outgoing
         // piece of every peer chunk to staging, then send it and receive in place
@@ -439,7 +470,6 @@ int do_swap(qsim *q) {
             NK(ncclGroupEnd());
         }
     }
-    q->parity ^= 1;
     return QSIM_OK;
 }
 
@@ -502,7 +532,7 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         q->res_valid = true;
         return QSIM_OK;
     }
-    std::vector<PassOp> ops = build_schedule((int)q->sets.size(), q->g, p, gam, bet, q->pending_plus);
+    std::vector<PassOp> ops = build_schedule((int)q->sets.size(), q->g, p, gam, bet, q->pending_plus, q->fused_swap);
     if (q->pending_plus) q->flip = 0;
     int last_grid = 0;
     for (const PassOp &op : ops) {
@@ -534,6 +564,12 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         P.reduce = op.reduce;
         P.gamma = op.gamma;
         P.rec = q->d_rec;
+        if (op.swap_fused) {
+            P.swap_store = 1;
+            P.gbits = q->g;
+            P.rank = q->rank;
+            for (int c = 0; c < q->world; ++c) P.dst[c] = q->peer[q->cur ^ 1][c];
+        }
         if (op.phase || op.reduce) {
             CK(qk::launch_tile_fields(P, q->d_rec, q->st));
             q->launches++;
@@ -555,6 +591,10 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
             q->prof_bytes.push_back((op.init ? 16.0 : 32.0) * (double)(1ull << q->m));
         }
         last_grid = grid;
+        if (op.swap_fused) {
+            int rc = finish_fused_swap(q);
+            if (rc) return rc;
+        }
         if (op.swap_after) {
             int rc = do_swap(q);
             if (rc) return rc;
@@ -691,6 +731,7 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
         ncclUniqueId id;
         std::memcpy(&id, uid, sizeof(id));
         NK(ncclCommInitRank(&q->comm, world, id, rank));
+        if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
         // out-of-place swap buffer when it leaves >= 8 GiB free, else in-place staging
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot));
@@ -699,6 +740,39 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
                 cudaGetLastError();
                 q->tmp = nullptr;
             }
+        }
+        CK(cudaMalloc(&q->d_bar, sizeof(double)));
+        CK(cudaMemsetAsync(q->d_bar, 0, sizeof(double), q->st));
+        // fused swap: map every rank's two state buffers (CUDA IPC handles all-gathered over NCCL)
+        const char *fz = std::getenv("QSIM_FUSED_SWAP");
+        if (q->tmp && !q->user_buf && q->use_tma && !(fz && std::atoi(fz) == 0)) {
+            q->bufs[0] = q->psi;
+            q->bufs[1] = q->tmp;
+            const size_t hs = sizeof(cudaIpcMemHandle_t);
+            std::vector<unsigned char> mine(2 * hs), all(2 * hs * world);
+            CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t *>(mine.data()), q->bufs[0]));
+            CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t *>(mine.data() + hs), q->bufs[1]));
+            unsigned char *dh = nullptr;
+            CK(cudaMalloc(&dh, all.size()));
+            CK(cudaMemcpyAsync(dh + (size_t)rank * 2 * hs, mine.data(), 2 * hs, cudaMemcpyHostToDevice, q->st));
+            NK(ncclAllGather(dh + (size_t)rank * 2 * hs, dh, 2 * hs, ncclUint8, q->comm, q->st));
+            CK(cudaMemcpyAsync(all.data(), dh, all.size(), cudaMemcpyDeviceToHost, q->st));
+            CK(cudaStreamSynchronize(q->st));
+            cudaFree(dh);
+            for (int c = 0; c < world; ++c)
+                for (int b = 0; b < 2; ++b) {
+                    if (c == rank) {
+                        q->peer[b][c] = q->bufs[b];
+                        continue;
+                    }
+                    cudaIpcMemHandle_t hnd;
+                    std::memcpy(&hnd, all.data() + ((size_t)c * 2 + b) * hs, hs);
+                    void *ptr = nullptr;
+                    CK(cudaIpcOpenMemHandle(&ptr, hnd, cudaIpcMemLazyEnablePeerAccess));
+                    q->peer[b][c] = (double2 *)ptr;
+                }
+            q->fused_swap = true;
+            q->cur = 0;
         }
     }
     q->pending_plus = true;
@@ -740,6 +814,16 @@ int qsim_create_ex(int n, int precision, int rank, int world, const void *nccl_u
 int qsim_destroy(qsim_t *q) {
     if (!q) return QSIM_EINVAL;
     if (q->st) cudaStreamSynchronize(q->st);
+    if (q->fused_swap) {
+        if (q->comm) {  // no rank may unmap while a peer could still write into it
+            ncclAllReduce(q->d_bar, q->d_bar, 1, ncclDouble, ncclSum, q->comm, q->st);
+            cudaStreamSynchronize(q->st);
+        }
+        for (int b = 0; b < 2; ++b)
+            for (int c = 0; c < q->world; ++c)
+                if (c != q->rank && q->peer[b][c]) cudaIpcCloseMemHandle(q->peer[b][c]);
+    }
+    if (q->d_bar) cudaFree(q->d_bar);
     if (q->comm) ncclCommDestroy(q->comm);
     if (q->psi && q->psi != q->user_buf) cudaFree(q->psi);
     if (q->tmp && q->tmp != q->user_buf) cudaFree(q->tmp);
@@ -921,9 +1005,9 @@ int qsim_plan_counts(int n, int world, int p, int *passes_out, int *swaps_out, u
         passes = 1;
     } else {
         std::vector<double> z(p, 0.0);
-        auto ops = build_schedule((int)build_sets(m).size(), g, p, z.data(), z.data(), true);
+        auto ops = build_schedule((int)build_sets(m).size(), g, p, z.data(), z.data(), true, g > 0);
         passes = (int)ops.size();
-        for (auto &o : ops) swaps += o.swap_after ? 1 : 0;
+        for (auto &o : ops) swaps += (o.swap_after || o.swap_fused) ? 1 : 0;
     }
     if (passes_out) *passes_out = passes;
     if (swaps_out) *swaps_out = swaps;

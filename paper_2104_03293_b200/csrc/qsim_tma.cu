@@ -131,6 +131,24 @@ __device__ __forceinline__ void wait_tile(const TmaIssue &I, u64 i) {
 
 constexpr unsigned TMX = 0xF80u, TMY = 0x01Fu, TMZ = 0x060u, TMW = 0x078u;
 
+// store with the fused global-qubit swap: local index x = (c | y) with c the top
+// g local bits goes to rank c's other buffer at (rank | y); 1/G of the stores stay local, the
+// rest cross NVLink as 16-byte stores coalesced into >= 128-byte rows.
+template <int F>
+__device__ __forceinline__ void store_tile_swapped(const double2 (&v)[NR], const PassParams &P, u64 xb) {
+    const int sh = P.m - P.gbits;
+    const u64 ymask = (1ull << sh) - 1ull;
+    const u64 rofs = (u64)P.rank << sh;
+    const u64 s0 = 1ull << P.L[Frame<F>::RB], s1 = 1ull << P.L[Frame<F>::RB + 1], s2 = 1ull << P.L[Frame<F>::RB + 2],
+              s3 = 1ull << P.L[Frame<F>::RB + 3], s4 = 1ull << P.L[Frame<F>::RB + 4];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+        const u64 x = xb + ((j & 1) ? s0 : 0) + ((j & 2) ? s1 : 0) + ((j & 4) ? s2 : 0) + ((j & 8) ? s3 : 0) +
+                      ((j & 16) ? s4 : 0);
+        __stcs(P.dst[x >> sh] + (rofs | (x & ymask)), v[j]);
+    }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(TMA_NG * 128, 1)
     tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassParams P) {
@@ -255,7 +273,8 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         // ------------------------------------------------ finish in registers, store
         if (TURN) {
             mix_frame<FX>(v, P.mix2 & TMX, P.c2.t);
-            store_tile<FX>(v, P.psi + tb + offX, P.L);
+            if (P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
+            else store_tile<FX>(v, P.psi + tb + offX, P.L);
         } else {
             if (RUN) mix_frame<FW>(v, P.mix1 & TMW, P.c1.t);
             else mix_frame<FZ>(v, P.mix1 & TMZ, P.c1.t);
@@ -273,6 +292,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             store_tile<RUN ? FW : FZ>(v, P.psi + tb + offS, P.L);
         }
     }
+    if (P.swap_store) __threadfence_system();  // NVLink stores visible before the pass completes
     if (P.reduce) {
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
