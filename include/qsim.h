@@ -157,7 +157,7 @@ int qsim_profile_read(qsim_t *q, double *ms_sum, uint64_t *count, double *bytes_
 
 /* Diagnostic micro-benchmark (modifies the state): time `reps` back-to-back launches of
  * the tile pass over tile set `set` (0 = bits 0..11, 1.. = the run sets in ascending bit
- * order) with phase on (1) / off (0) / no butterflies at all (-1, a pure streaming copy of
+ * order, one past the last = the relabelling schedule's out-of-place tile shape) with phase on (1) / off (0) / no butterflies at all (-1, a pure streaming copy of
  * the same access pattern), on the handle's stream; *ms_out = mean ms per launch. */
 int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out);
 

@@ -59,6 +59,14 @@ struct PassParams {
     // dst[c][(rank << (m-g)) | y] (dst[c] = rank c's other state buffer, mapped over NVLink)
     int swap_store, gbits, rank;
     double2 *dst[8];
+    int dbg;             // diagnostics (qsim_bench_pass): bit 0 skip stores, bit 1 skip state loads
+    int tma_store;       // store tiles with TMA from the stage instead of STG from registers
+    // out-of-place tile-major store (single-GPU relabelling schedule): tile u goes to the
+    // contiguous block out + (out_u << 12), out_u = sum_s ((u >> src_s) & (2^len_s - 1)) << dst_s
+    int tmo;
+    double2 *out;
+    int onseg;
+    int oseg_src[20], oseg_len[20], oseg_dst[20];
 };
 
 constexpr size_t TILE_REC_BYTES = 320;  // sizeof(TileRec)

@@ -255,9 +255,16 @@ struct qsim {
     ncclComm_t comm = nullptr;
     bool has_ising = false;
     std::vector<double> h, J;  // logical, J symmetric with zero diagonal
-    int parity = 0;            // number of swaps mod 2 (permutation state)
+    int pos[qk::NMAX];         // logical qubit -> physical bit position (the paper's permutation array)
+    int qat[qk::NMAX];         // physical bit position -> logical qubit
     u64 flip = 0;              // index flip mask F: physical x holds the amplitude of x ^ F
-    double *d_hp[2] = {nullptr, nullptr}, *d_Jp[2] = {nullptr, nullptr};
+    static constexpr int NFR = 4;
+    double *d_fr[NFR] = {};    // ring of physical-frame (h, J) copies: hp[n] then Jp[n*n]
+    int fr_slot = 0;
+    bool fr_valid = false;     // d_fr[fr_slot] matches pos[]
+    const double *cur_hp = nullptr, *cur_Jp = nullptr;
+    bool tilemajor = false;    // single GPU: out-of-place relabelling schedule (second buffer)
+    TileSet tmset;             // its fixed tile shape: bits {0,1,2} + {12..20}
     double *d_part = nullptr, *d_res = nullptr, *d_ang = nullptr;
     size_t ang_cap = 0;
     void *d_scratch = nullptr;
@@ -269,6 +276,8 @@ struct qsim {
     uint64_t launches = 0;
     int prefetch = 1;          // L2 prefetch of the next tile (QSIM_PREFETCH=0 disables, for experiments)
     int use_tma = 1;           // TMA-pipelined pass kernel (QSIM_KERNEL=v4 selects the register-direct one)
+    int l2promo = (int)CU_TENSOR_MAP_L2_PROMOTION_L2_128B;  // TMA L2 sector promotion (QSIM_L2PROMO=0..3)
+    int tma_store = 1;         // TMA stores from the stage (QSIM_TMA_STORE=0: STG from registers)
     std::string err;
     // optional per-pass timing (CUDA events on the handle's stream around each pass launch)
     bool prof = false;
@@ -312,6 +321,44 @@ int phys_pos(int n, int m, int g, int par, int qb) {
     return qb;
 }
 
+void reset_perm(qsim *q) {
+    for (int i = 0; i < q->n; ++i) q->pos[i] = q->qat[i] = i;
+    q->flip = 0;
+    q->fr_valid = false;
+}
+
+// relabel the qubits: the qubit at physical position x moves to position newp[x] (data moved
+// by the pass that realises it); the flip mask's bits travel with the qubits
+void relabel(qsim *q, const int *newp) {
+    for (int a = 0; a < q->n; ++a) q->pos[a] = newp[q->pos[a]];
+    for (int a = 0; a < q->n; ++a) q->qat[q->pos[a]] = a;
+    u64 f = 0;
+    for (int x = 0; x < q->n; ++x)
+        if ((q->flip >> x) & 1ull) f |= 1ull << newp[x];
+    q->flip = f;
+    q->fr_valid = false;
+}
+
+// make cur_hp / cur_Jp the physical-frame copy of (h, J) for the current permutation
+// (stream-ordered upload into the next ring slot; older slots stay valid for queued kernels)
+int ensure_frame(qsim *q) {
+    if (q->fr_valid) return QSIM_OK;
+    const int n = q->n;
+    std::vector<double> fr((size_t)n + (size_t)n * n, 0.0);
+    for (int a = 0; a < n; ++a) {
+        const int pa = q->pos[a];
+        fr[pa] = q->h[a];
+        for (int b = 0; b < n; ++b) fr[n + (size_t)pa * n + q->pos[b]] = q->J[(size_t)a * n + b];
+    }
+    const int slot = (q->fr_slot + 1) % qsim::NFR;
+    CK(cudaMemcpyAsync(q->d_fr[slot], fr.data(), sizeof(double) * fr.size(), cudaMemcpyHostToDevice, q->st));
+    q->fr_slot = slot;
+    q->cur_hp = q->d_fr[slot];
+    q->cur_Jp = q->d_fr[slot] + n;
+    q->fr_valid = true;
+    return QSIM_OK;
+}
+
 int scratch(qsim *q, size_t bytes) {
     if (q->scratch_cap >= bytes) return QSIM_OK;
     if (q->d_scratch) cudaFree(q->d_scratch);
@@ -328,7 +375,7 @@ int materialize_plus(qsim *q) {
     CK(qk::launch_init_plus(q->psi, 1ull << q->m, a0, q->num_sms * 8, q->st));
     q->launches++;
     q->pending_plus = false;
-    q->flip = 0;
+    reset_perm(q);  // |+>^n is invariant under qubit relabelling
     q->res_valid = false;
     return QSIM_OK;
 }
@@ -336,8 +383,8 @@ int materialize_plus(qsim *q) {
 qk::PassParams base_params(qsim *q, const TileSet &S) {
     qk::PassParams P{};
     P.psi = q->psi;
-    P.hp = q->d_hp[q->parity];
-    P.Jp = q->d_Jp[q->parity];
+    P.hp = q->cur_hp;
+    P.Jp = q->cur_Jp;
     P.n = q->n;
     P.m = q->m;
     P.xglob = (u64)q->rank << q->m;
@@ -355,6 +402,7 @@ qk::PassParams base_params(qsim *q, const TileSet &S) {
     // L2 prefetch pays only for the contiguous 64 KiB tiles of the 12-bit set; for run sets
     // every tile touches up to 512 distinct 2 MiB pages and prefetching slows them (measured)
     P.prefetch = q->prefetch && S.full12;
+    P.tma_store = q->tma_store;
     return P;
 }
 
@@ -379,7 +427,7 @@ int launch_pass_any(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out)
         cuuint32_t es[5] = {1, 1, 1, 1, 1};
         CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5u, (void *)q->psi, S.tm_dim,
                          S.tm_stride + 1, S.tm_box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         (CUtensorMapL2promotion)q->l2promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
         for (int d = 0; d < 5; ++d) {
             P.tm_clen[d] = S.tm_clen[d];
@@ -405,14 +453,11 @@ int finish_reduce(qsim *q, int nparts) {
     return QSIM_OK;
 }
 
-// bookkeeping of a swap of positions [m-g, m) <-> [m, n): permutation parity and the flip
-// mask (its bits travel with the qubits)
+// bookkeeping of a swap of positions [m-g, m) <-> [m, n): permutation and flip mask
 void swap_bookkeeping(qsim *q) {
-    const u64 gm = (1ull << q->g) - 1ull;
-    const u64 lo = (q->flip >> (q->m - q->g)) & gm, hi = (q->flip >> q->m) & gm;
-    q->flip &= ~((gm << (q->m - q->g)) | (gm << q->m));
-    q->flip |= (hi << (q->m - q->g)) | (lo << q->m);
-    q->parity ^= 1;
+    int newp[qk::NMAX];
+    for (int x = 0; x < q->n; ++x) newp[x] = phys_pos(q->n, q->m, q->g, 1, x);
+    relabel(q, newp);
 }
 
 // after a fused swap pass: wait until every rank's pass (and its NVLink stores) is done, then
@@ -485,23 +530,15 @@ int prof_events(qsim *q, cudaEvent_t *a, cudaEvent_t *b) {
     return QSIM_OK;
 }
 
-int upload_frames(qsim *q) {
-    const int n = q->n;
-    for (int par = 0; par < (q->g ? 2 : 1); ++par) {
-        std::vector<double> hp(n), Jp((size_t)n * n, 0.0);
-        for (int a = 0; a < n; ++a) {
-            int pa = phys_pos(n, q->m, q->g, par, a);
-            hp[pa] = q->h[a];
-            for (int b = 0; b < n; ++b) Jp[(size_t)pa * n + phys_pos(n, q->m, q->g, par, b)] = q->J[(size_t)a * n + b];
-        }
-        CK(cudaMemcpyAsync(q->d_hp[par], hp.data(), sizeof(double) * n, cudaMemcpyHostToDevice, q->st));
-        CK(cudaMemcpyAsync(q->d_Jp[par], Jp.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, q->st));
-    }
-    CK(cudaStreamSynchronize(q->st));
-    return QSIM_OK;
-}
+int apply_tilemajor(qsim *q, const double *gam, const double *bet, int p);
 
 int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
+    if (q->pending_plus) reset_perm(q);  // the first pass writes |+>^n: any labelling is valid
+    {
+        int rc = ensure_frame(q);
+        if (rc) return rc;
+    }
+    if (q->tilemajor) return apply_tilemajor(q, gam, bet, p);
     if (q->m <= qk::KT) {  // whole state in one CTA (single GPU only)
         if ((size_t)2 * p > q->ang_cap) {
             if (q->d_ang) cudaFree(q->d_ang);
@@ -515,8 +552,8 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         CK(cudaMemcpyAsync(q->d_ang, ang.data(), sizeof(double) * 2 * p, cudaMemcpyHostToDevice, q->st));
         qk::SmallParams S{};
         S.psi = q->psi;
-        S.hp = q->d_hp[0];
-        S.Jp = q->d_Jp[0];
+        S.hp = q->cur_hp;
+        S.Jp = q->cur_Jp;
         S.ang = q->d_ang;
         S.n = q->n;
         S.p = p;
@@ -533,10 +570,13 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         return QSIM_OK;
     }
     std::vector<PassOp> ops = build_schedule((int)q->sets.size(), q->g, p, gam, bet, q->pending_plus, q->fused_swap);
-    if (q->pending_plus) q->flip = 0;
     int last_grid = 0;
     for (const PassOp &op : ops) {
         const TileSet &S = q->sets[op.set];
+        {
+            int rc = ensure_frame(q);  // a swap may have relabelled the qubits
+            if (rc) return rc;
+        }
         qk::PassParams P = base_params(q, S);
         std::complex<double> k1(1.0, 0.0), k2(1.0, 0.0);
         const unsigned m1 = op.mix1 & S.own, m2 = op.mix2 & S.own;
@@ -604,6 +644,149 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
     return finish_reduce(q, last_grid);
 }
 
+// Single-GPU relabelling schedule (m >= 21, needs a second state buffer).  Every
+// pass reads tiles of the fixed shape L = {0,1,2} + {12..20} (TMA: 128-byte rows at a 64 KiB
+// stride, 16 pages per tile) and writes each tile as one contiguous 64 KiB block of the other
+// buffer.  Writing the tile bits to positions 0..11 and the tile-id bits in a chosen order is a
+// qubit relabelling; it is chosen so that the next pass's qubits sit at positions 12.. .  Groups
+// (from the layout at entry): 0 = the qubits at 0..11 (mixed together, all 12 tile bits), 1..K =
+// the runs over 12..m-1 (<= 9 each, balanced).  Passes follow the same boustrophedon as
+// build_schedule ((K) p + 1 passes); a run shorter than 9 fills its tile with "filler" qubits
+// of a run that is neither this pass's nor the next pass's.
+int apply_tilemajor(qsim *q, const double *gam, const double *bet, int p) {
+    const int n = q->n, m = q->m;
+    const TileSet &S = q->tmset;
+    const int R = m - qk::KT;
+    const int K = (R + 8) / 9;
+    std::vector<int> gid(n, -1);
+    for (int x = 0; x < qk::KT; ++x) gid[q->qat[x]] = 0;
+    {
+        int x = qk::KT;
+        for (int k = 1; k <= K; ++k) {
+            const int len = R / K + (k <= R % K ? 1 : 0);
+            for (int i = 0; i < len; ++i) gid[q->qat[x++]] = k;
+        }
+    }
+    std::vector<PassOp> ops = build_schedule(K + 1, 0, p, gam, bet, q->pending_plus, false);
+    bool tile_pos[qk::NMAX] = {};
+    for (int t = 0; t < qk::KT; ++t) tile_pos[S.L[t]] = true;
+    int last_grid = 0;
+    for (size_t i = 0; i < ops.size(); ++i) {
+        const PassOp &op = ops[i];
+        const int gi = op.set;
+        const int gn = i + 1 < ops.size() ? ops[i + 1].set : -1;
+        const int gnn = i + 2 < ops.size() ? ops[i + 2].set : -1;
+        int rc = ensure_frame(q);
+        if (rc) return rc;
+        // tile bits of this pass that hold its group's qubits
+        unsigned own = 0;
+        for (int t = 0; t < qk::KT; ++t)
+            if (gid[q->qat[S.L[t]]] == gi) own |= 1u << t;
+        if (gi > 0)  // a run: its qubits must be at the top-of-tile positions 12..
+            for (int t = 0; t < 3; ++t)
+                if ((own >> t) & 1u) return fail(q, QSIM_ECUDA, "relabel plan: run qubit at a passenger position");
+        // ---- output labelling: tile bit t -> position t; tile-id qubits -> 12.. with the next
+        // group first, then its fillers, then the rest in ascending position
+        int newp[qk::NMAX];
+        for (int t = 0; t < qk::KT; ++t) newp[S.L[t]] = t;
+        std::vector<int> ids;  // non-tile positions ascending (= tile-id bit order)
+        for (int x = 0; x < m; ++x)
+            if (!tile_pos[x]) ids.push_back(x);
+        std::vector<bool> placed(m, false);
+        int nextp = qk::KT;
+        if (gn >= 0) {
+            for (int x : ids)
+                if (gid[q->qat[x]] == gn) {
+                    newp[x] = nextp++;
+                    placed[x] = true;
+                }
+            const int need = gn > 0 ? qk::KT + 9 - nextp : 0;
+            int got = 0;
+            for (int x : ids) {
+                if (got >= need) break;
+                const int gx = gid[q->qat[x]];
+                if (placed[x] || gx == 0 || gx == gn || gx == gnn) continue;
+                newp[x] = nextp++;
+                placed[x] = true;
+                ++got;
+            }
+            if (got < need) return fail(q, QSIM_ECUDA, "relabel plan: not enough filler qubits");
+            // the next group must be entirely in this pass's tile-id bits
+            for (int t = 0; t < qk::KT; ++t)
+                if (gn > 0 && gid[q->qat[S.L[t]]] == gn) return fail(q, QSIM_ECUDA, "relabel plan: next group in tile");
+            for (int t = 3; t < qk::KT; ++t)
+                if (gn == 0 && gid[q->qat[S.L[t]]] == 0 && S.L[t] >= qk::KT)
+                    return fail(q, QSIM_ECUDA, "relabel plan: next group in tile");
+        }
+        for (int x : ids)
+            if (!placed[x]) newp[x] = nextp++;
+        // output tile id segments: tile-id bit k (position ids[k]) -> bit newp[ids[k]] - 12
+        qk::PassParams P = base_params(q, S);
+        P.onseg = 0;
+        for (size_t k = 0; k < ids.size();) {
+            size_t e = k + 1;
+            while (e < ids.size() && newp[ids[e]] == newp[ids[e - 1]] + 1) ++e;
+            if (P.onseg == 20) return fail(q, QSIM_ECUDA, "relabel plan: too many segments");
+            P.oseg_src[P.onseg] = (int)k;
+            P.oseg_len[P.onseg] = (int)(e - k);
+            P.oseg_dst[P.onseg] = newp[ids[k]] - qk::KT;
+            ++P.onseg;
+            k = e;
+        }
+        P.tmo = 1;
+        P.out = q->bufs[q->cur ^ 1];
+        P.prefetch = 0;
+        // ---- mixing, phase, flips (as in the in-place schedule)
+        std::complex<double> k1(1.0, 0.0), k2(1.0, 0.0);
+        P.c1 = mix_coef(op.b1, k1);
+        P.c2 = mix_coef(op.b2, k2);
+        P.mix1 = op.mix1 & own;
+        P.mix2 = op.phase ? (op.mix2 & own) : 0u;
+        std::complex<double> sc = cpow_int(k1, __builtin_popcount(P.mix1)) * cpow_int(k2, __builtin_popcount(P.mix2));
+        P.scale = make_double2(sc.real(), sc.imag());
+        auto posmask = [&](unsigned tm) {
+            u64 r = 0;
+            for (int t = 0; t < qk::KT; ++t)
+                if ((tm >> t) & 1u) r |= 1ull << S.L[t];
+            return r;
+        };
+        const u64 f1 = P.c1.form ? posmask(P.mix1) : 0ull;
+        const u64 f2 = P.c2.form ? posmask(P.mix2) : 0ull;
+        P.flip = q->flip ^ f1;
+        q->flip = P.flip ^ f2;
+        P.kind = gi == 0 ? (op.phase ? qk::K_TURN12 : qk::K_PLAIN12) : (op.phase ? qk::K_TURN_RUN : qk::K_PLAIN_RUN);
+        P.init = op.init;
+        P.phase = op.phase;
+        P.reduce = op.reduce;
+        P.gamma = op.gamma;
+        P.rec = q->d_rec;
+        if (op.phase || op.reduce) {
+            CK(qk::launch_tile_fields(P, q->d_rec, q->st));
+            q->launches++;
+        }
+        int grid = 0;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (q->prof) {
+            rc = prof_events(q, &e0, &e1);
+            if (rc) return rc;
+            CK(cudaEventRecord(e0, q->st));
+        }
+        rc = launch_pass_any(q, S, P, &grid);
+        if (rc) return rc;
+        if (q->prof) {
+            CK(cudaEventRecord(e1, q->st));
+            q->prof_bytes.push_back((op.init ? 16.0 : 32.0) * (double)(1ull << m));
+        }
+        last_grid = grid;
+        relabel(q, newp);
+        q->cur ^= 1;
+        q->psi = q->bufs[q->cur];
+        q->tmp = q->bufs[q->cur ^ 1];
+    }
+    q->pending_plus = false;
+    return finish_reduce(q, last_grid);
+}
+
 int check_angles(const double *a, int p) {
     for (int i = 0; i < p; ++i)
         if (!std::isfinite(a[i])) return QSIM_EINVAL;
@@ -613,12 +796,14 @@ int check_angles(const double *a, int p) {
 int run_reduce(qsim *q) {
     int rc = materialize_plus(q);
     if (rc) return rc;
+    rc = ensure_frame(q);
+    if (rc) return rc;
     if (q->res_valid) return QSIM_OK;
     if (q->m <= qk::KT) {
         qk::SmallParams S{};
         S.psi = q->psi;
-        S.hp = q->d_hp[0];
-        S.Jp = q->d_Jp[0];
+        S.hp = q->cur_hp;
+        S.Jp = q->cur_Jp;
         S.ang = nullptr;
         S.n = q->n;
         S.p = 0;
@@ -630,7 +815,7 @@ int run_reduce(qsim *q) {
         q->res_valid = true;
         return QSIM_OK;
     }
-    const TileSet &S = q->sets[0];
+    const TileSet &S = q->tilemajor ? q->tmset : q->sets[0];
     qk::PassParams P = base_params(q, S);
     P.rec = q->d_rec;
     P.flip = q->flip;
@@ -651,7 +836,7 @@ qk::GatherParams gather_params(const qsim *q, u64 first, u64 count, const u64 *l
     G.count = count;
     G.list = list;
     G.flip = q->flip;
-    for (int b = 0; b < q->n; ++b) G.pos[b] = (unsigned char)phys_pos(q->n, q->m, q->g, q->parity, b);
+    for (int b = 0; b < q->n; ++b) G.pos[b] = (unsigned char)q->pos[b];
     return G;
 }
 
@@ -717,15 +902,38 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
         }
         q->own_psi = true;
     }
-    for (int par = 0; par < 2; ++par) {
-        CK(cudaMalloc(&q->d_hp[par], sizeof(double) * n));
-        CK(cudaMalloc(&q->d_Jp[par], sizeof(double) * n * n));
-    }
+    for (int k = 0; k < qsim::NFR; ++k) CK(cudaMalloc(&q->d_fr[k], sizeof(double) * ((size_t)n + (size_t)n * n)));
+    reset_perm(q);
     CK(cudaMalloc(&q->d_part, sizeof(double) * 2 * 4 * q->num_sms));
     CK(cudaMalloc(&q->d_res, sizeof(double) * 2));
     if (q->m > qk::KT) {
         q->sets = build_sets(q->m);
         CK(cudaMalloc(&q->d_rec, qk::TILE_REC_BYTES << (q->m - qk::KT)));
+    }
+    if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
+    if (world == 1 && q->m >= qk::KT + 9 && q->use_tma && !buf) {
+        // relabelling schedule: needs a second buffer (kept only if >= 8 GiB stay free)
+        // (measured slower than the in-place schedule on B200: concurrent scattered reads and
+        // contiguous writes stream at ~84 % while either alone runs at ~98 %; opt-in only)
+        const char *tz = std::getenv("QSIM_TILEMAJOR");
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        if (tz && std::atoi(tz) == 1 && fr > bytes + (8ull << 30)) {
+            if (cudaMalloc(&q->tmp, bytes) == cudaSuccess) {
+                std::vector<int> L;
+                for (int i = 0; i < 3; ++i) L.push_back(i);
+                for (int i = qk::KT; i < qk::KT + 9; ++i) L.push_back(i);
+                q->tmset = make_set(q->m, L, (1u << qk::KT) - 1);
+                q->tmset.full12 = false;
+                q->bufs[0] = q->psi;
+                q->bufs[1] = q->tmp;
+                q->cur = 0;
+                q->tilemajor = q->tmset.tm_ok;
+            } else {
+                cudaGetLastError();
+                q->tmp = nullptr;
+            }
+        }
     }
     if (world > 1) {
         ncclUniqueId id;
@@ -777,6 +985,8 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     }
     q->pending_plus = true;
     if (const char *e = std::getenv("QSIM_PREFETCH")) q->prefetch = std::atoi(e);
+    if (const char *e = std::getenv("QSIM_L2PROMO")) q->l2promo = std::atoi(e);
+    if (const char *e = std::getenv("QSIM_TMA_STORE")) q->tma_store = std::atoi(e);
     if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
     if (q->use_tma) {
         CK(qk::setup_tma_kernels());
@@ -827,10 +1037,8 @@ int qsim_destroy(qsim_t *q) {
     if (q->comm) ncclCommDestroy(q->comm);
     if (q->psi && q->psi != q->user_buf) cudaFree(q->psi);
     if (q->tmp && q->tmp != q->user_buf) cudaFree(q->tmp);
-    for (int par = 0; par < 2; ++par) {
-        if (q->d_hp[par]) cudaFree(q->d_hp[par]);
-        if (q->d_Jp[par]) cudaFree(q->d_Jp[par]);
-    }
+    for (int k = 0; k < qsim::NFR; ++k)
+        if (q->d_fr[k]) cudaFree(q->d_fr[k]);
     if (q->d_part) cudaFree(q->d_part);
     if (q->d_res) cudaFree(q->d_res);
     if (q->d_ang) cudaFree(q->d_ang);
@@ -858,7 +1066,8 @@ int qsim_set_ising(qsim_t *q, const double *h, const double *J) {
     }
     q->h = hh;
     q->J = JJ;
-    int rc = upload_frames(q);
+    q->fr_valid = false;
+    int rc = ensure_frame(q);
     if (rc) return rc;
     q->has_ising = true;
     q->res_valid = false;
@@ -967,6 +1176,10 @@ int qsim_energies(qsim_t *q, uint64_t first, uint64_t count, double *out) {
     if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
     if (count == 0) return QSIM_OK;
     if (first >> q->n || count > (1ull << q->n) - first) return fail(q, QSIM_ERANGE, "range exceeds 2^n");
+    {
+        int rc = ensure_frame(q);
+        if (rc) return rc;
+    }
     qk::ProbeSet PS{};
     PS.k = std::min(qk::KT, q->m);
     PS.lmask = 0;
@@ -980,7 +1193,7 @@ int qsim_energies(qsim_t *q, uint64_t first, uint64_t count, double *out) {
         int rc = scratch(q, c * sizeof(double));
         if (rc) return rc;
         qk::GatherParams G = gather_params(q, first + done, c, nullptr);
-        CK(qk::launch_energy_probe(G, q->d_hp[q->parity], q->d_Jp[q->parity], PS, (double *)q->d_scratch,
+        CK(qk::launch_energy_probe(G, q->cur_hp, q->cur_Jp, PS, (double *)q->d_scratch,
                                    (int)std::min<u64>((c + 255) / 256, 4096), q->st));
         q->launches++;
         CK(cudaMemcpyAsync(out + done, q->d_scratch, c * sizeof(double), cudaMemcpyDeviceToHost, q->st));
@@ -1025,21 +1238,39 @@ int qsim_plan_positions(int n, int world, int layers, int *pos_out) {
 
 int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
     if (!q || !ms_out || reps < 1) return QSIM_EINVAL;
-    if (q->m <= qk::KT || set < 0 || set >= (int)q->sets.size()) return fail(q, QSIM_EINVAL, "no such tile set");
+    const int ns = (int)q->sets.size();
+    const bool tm = q->tilemajor && set == ns;  // the relabelling schedule's tile shape, out of place
+    if (q->m <= qk::KT || set < 0 || set > ns || (set == ns && !tm)) return fail(q, QSIM_EINVAL, "no such tile set");
     if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
     int rc = materialize_plus(q);
     if (rc) return rc;
-    const TileSet &S = q->sets[set];
+    rc = ensure_frame(q);
+    if (rc) return rc;
+    const TileSet &S = tm ? q->tmset : q->sets[set];
     qk::PassParams P = base_params(q, S);
+    if (tm) {  // identity output labelling
+        P.tmo = 1;
+        P.out = q->bufs[q->cur ^ 1];
+        P.onseg = 1;
+        P.oseg_src[0] = 0;
+        P.oseg_len[0] = q->m - qk::KT;
+        P.oseg_dst[0] = 0;
+    }
     std::complex<double> k1, k2;
     P.c1 = mix_coef(0.3, k1);
     P.c2 = mix_coef(-0.2, k2);
-    P.mix1 = phase < 0 ? 0u : S.own;  // phase < 0: copy only (memory-pattern probe)
+    // phase < 0: memory-pattern probes: -1 copy, -2 read only, -3 write only (no butterflies)
+    P.mix1 = phase < 0 ? 0u : S.own;
     P.mix2 = phase > 0 ? S.own : 0u;
+    P.dbg = phase == -2 ? 1 : (phase == -3 ? 2 : 0);
     if (phase < 0) phase = 0;
     std::complex<double> sc = cpow_int(k1, __builtin_popcount(P.mix1)) * cpow_int(k2, __builtin_popcount(P.mix2));
     P.scale = make_double2(sc.real(), sc.imag());
     P.kind = S.full12 ? (phase ? qk::K_TURN12 : qk::K_PLAIN12) : (phase ? qk::K_TURN_RUN : qk::K_PLAIN_RUN);
+    if (tm) {  // tile-major shape: run passes mix t3..t11; the "12" program mixes all 12
+        P.mix1 = P.mix1 ? 0xFF8u : 0u;
+        P.mix2 = P.mix2 ? 0xFF8u : 0u;
+    }
     P.phase = phase;
     P.gamma = 0.1;
     P.rec = q->d_rec;

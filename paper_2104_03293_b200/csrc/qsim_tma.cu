@@ -67,6 +67,20 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
         "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap *tm, const int (&c)[5], const void *src) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+            reinterpret_cast<uint64_t>(tm)),
+        "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(src))
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tile_coords(const PassParams &P, u64 ut, int (&c)[5]) {
+#pragma unroll
+    for (int d = 0; d < 5; ++d)
+        c[d] = P.tm_clen[d] ? (int)((ut >> P.tm_cshift[d]) & ((1ull << P.tm_clen[d]) - 1ull)) : 0;
+}
 __device__ __forceinline__ void group_bar(int g) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(128) : "memory");
 }
@@ -131,6 +145,18 @@ __device__ __forceinline__ void wait_tile(const TmaIssue &I, u64 i) {
 
 constexpr unsigned TMX = 0xF80u, TMY = 0x01Fu, TMZ = 0x060u, TMW = 0x078u;
 
+// tile-major out-of-place store: the tile is written as one contiguous 64 KiB block (element
+// t at t), so every warp store covers >= 128 contiguous bytes and every CTA writes whole blocks
+template <int F>
+__device__ __forceinline__ void store_tile_major(const double2 (&v)[NR], const PassParams &P, u64 ut, int lane,
+                                                 int warp) {
+    u64 ou = 0;
+    for (int k = 0; k < P.onseg; ++k) ou |= ((ut >> P.oseg_src[k]) & ((1ull << P.oseg_len[k]) - 1ull)) << P.oseg_dst[k];
+    double2 *base = P.out + (ou << KT) + Frame<F>::tthr(lane, warp);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) __stcs(base + (j << Frame<F>::RB), v[j]);
+}
+
 // store with the fused global-qubit swap: local index x = (c | y) with c the top
 // g local bits goes to rank c's other buffer at (rank | y); 1/G of the stores stay local, the
 // rest cross NVLink as 16-byte stores coalesced into >= 128-byte rows.
@@ -165,7 +191,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     const int tid = threadIdx.x, g = tid >> 7, gt = tid & 127, lane = gt & 31, warp = gt >> 5;
     const int n = P.n;
     const bool need_e = TURN || P.reduce;
-    const bool load_state = !(TURN && P.init);
+    const bool load_state = !(TURN && P.init) && !(P.dbg & 2);
     const u64 ntl = (P.ntiles > blockIdx.x) ? (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     volatile int *issued = reinterpret_cast<volatile int *>(smem + TmaSmem::iss_off);
     const TmaIssue I{&tmap, reinterpret_cast<const TileRec *>(P.rec), stages, srec, full, issued};
@@ -263,7 +289,9 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         }
         // ------------------------------------------------ release the stage, refill it
         // (a reducing pass reads the stage's tile record, so it finishes before the refill)
-        const bool late_release = !TURN && P.reduce;
+        // TMA-store mode keeps the stage until the store has read it back
+        const bool tstore = P.tma_store && !P.swap_store && !P.tmo && !(P.dbg & 1);
+        const bool late_release = (!TURN && P.reduce) || tstore;
         if (!late_release) {
             fence_async_smem();
             group_bar(g);
@@ -274,22 +302,56 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         if (TURN) {
             mix_frame<FX>(v, P.mix2 & TMX, P.c2.t);
             if (P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
-            else store_tile<FX>(v, P.psi + tb + offX, P.L);
+            else if (P.tmo) store_tile_major<FX>(v, P, ut, lane, warp);
+            else if (tstore) {
+                sts_frame<FX>(v, sm, lane, warp);
+                fence_async_smem();
+                group_bar(g);
+                if (gt == 0) {
+                    int c[5];
+                    tile_coords(P, ut, c);
+                    tma_store_5d(I.tm, c, sm);
+                    bulk_wait_read0();
+                    if (i + NSTAGE < ntl) issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                }
+            } else
+                store_tile<FX>(v, P.psi + tb + offX, P.L);
         } else {
             if (RUN) mix_frame<FW>(v, P.mix1 & TMW, P.c1.t);
             else mix_frame<FZ>(v, P.mix1 & TMZ, P.c1.t);
+            if (P.dbg & 1) {  // diagnostics: read-only pass (keep the values alive)
+                double s = 0.0;
+#pragma unroll
+                for (int j = 0; j < NR; ++j) s += v[j].x;
+                if (s == 12345.678) P.psi[0] = v[0];
+                continue;
+            }
             if (P.scale.x != 1.0 || P.scale.y != 0.0) {
 #pragma unroll
                 for (int j = 0; j < NR; ++j) v[j] = cmul(v[j], P.scale);
             }
             if (P.reduce) accumulate<FE>(v, R, tE, fr, te, cs.eRR, acc_e, acc_n);
+            if (tstore) {
+                sts_frame<RUN ? FW : FZ>(v, sm, lane, warp);
+                fence_async_smem();
+                group_bar(g);
+                if (gt == 0) {
+                    int c[5];
+                    tile_coords(P, ut, c);
+                    tma_store_5d(I.tm, c, sm);
+                    bulk_wait_read0();
+                    if (i + NSTAGE < ntl) issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                }
+                continue;
+            }
             if (late_release) {
                 fence_async_smem();
                 group_bar(g);
                 if (gt == 0 && i + NSTAGE < ntl)
                     issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
             }
-            store_tile<RUN ? FW : FZ>(v, P.psi + tb + offS, P.L);
+            if (P.tmo) store_tile_major<RUN ? FW : FZ>(v, P, ut, lane, warp);
+            else store_tile<RUN ? FW : FZ>(v, P.psi + tb + offS, P.L);
         }
     }
     if (P.swap_store) __threadfence_system();  // NVLink stores visible before the pass completes

@@ -20,10 +20,11 @@ for n in a.n:
     h, J = inst.random_ising(n, 1)
     with Q.QSim(n) as s:
         s.set_ising(h, J)
-        nsets = 1 + -(-(n - 12) // 9)
+        nsets = 1 + -(-(n - 12) // 9) + (1 if n >= 21 else 0)  # + the tile-major shape
         ideal = 32 * 2.0 ** n / 6455.9e9 * 1e3
         for k in range(nsets):
-            for ph in (-1, 0, 1):
+            for ph in (-3, -2, -1, 0, 1):
                 ms = Q.qsim_bench_pass(s.h, k, ph, a.reps)
-                print(f"n={n} set={k} phase={ph} {ms:.3f} ms  ({ideal / ms * 100:.1f}% of measured HBM peak)",
+                fac = 0.5 if ph in (-2, -3) else 1.0  # read-only / write-only move half the bytes
+                print(f"n={n} set={k} phase={ph} {ms:.3f} ms  ({fac * ideal / ms * 100:.1f}% of measured HBM peak)",
                       flush=True)
