@@ -941,9 +941,11 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
         NK(ncclCommInitRank(&q->comm, world, id, rank));
         if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
         // out-of-place swap buffer when it leaves >= 8 GiB free, else in-place staging
+        // (QSIM_SWAP_INPLACE=1 forces the in-place path, for tests)
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot));
-        if (fr > bytes + (8ull << 30)) {
+        const char *ip = std::getenv("QSIM_SWAP_INPLACE");
+        if (fr > bytes + (8ull << 30) && !(ip && std::atoi(ip) == 1)) {
             if (cudaMalloc(&q->tmp, bytes) != cudaSuccess) {
                 cudaGetLastError();
                 q->tmp = nullptr;
