@@ -129,6 +129,26 @@ int qsim_get_amplitudes(qsim_t *q, uint64_t first, uint64_t count, double *out);
  * the same tile-factorised energy arithmetic the cost-phase kernel uses. */
 int qsim_energies(qsim_t *q, uint64_t first, uint64_t count, double *out);
 
+/* spin expectations <sigma^z_i> = sum_z |psi_z|^2 s_i(z), i = 0..n-1 in
+ * logical order ("spin expectation values during the time evolution"; Fig. 5). */
+int qsim_spin_expectations(qsim_t *q, double *out);
+
+/* qsim_apply_aqa that also records <sigma^z_i> after every layer k into trace[k*n + i]
+ * (p*n doubles).  Layers are applied one at a time (P passes per layer instead of P-1). */
+int qsim_apply_aqa_traced(qsim_t *q, double T, int p, const double *s, const double *A, const double *B,
+                          int n_knots, double *trace);
+
+/* full enumeration of E(z) over all 2^n labels on the GPU(s) (the paper's
+ * t_FE): the minimum energy, the number of minimisers, and the first
+ * max_out minimisers in ascending label order.  Needs n >= 12.  Independent of the state. */
+int qsim_ground_states(qsim_t *q, uint64_t *out, int max_out, double *emin, uint64_t *count);
+
+/* State-less variant on the current device (no 2^n state is allocated, so n may exceed
+ * what fits in memory, 12 <= n <= 48): same results as qsim_ground_states, plus the
+ * device time in *ms_out (optional).  Errors are reported by qsim_last_error(NULL). */
+int qsim_enumerate(int n, const double *h, const double *J, uint64_t *out, int max_out, double *emin,
+                   uint64_t *count, double *ms_out);
+
 /* Wait for all work enqueued on the handle's stream. */
 int qsim_sync(qsim_t *q);
 

@@ -69,6 +69,19 @@ def p1_path_amplitude(h, J, gamma: float, beta: float, z: int) -> complex:
 #                              - cos(2g(h_u+h_v)) prod_{w!=u,v} cos(2g(J_uw+J_vw))]
 # <H_C> = sum_u h_u <s_u> + sum_{u<v} J_uv <s_u s_v>.
 # ---------------------------------------------------------------------------------
+def p1_spins(h, J, gamma: float, beta: float) -> np.ndarray:
+    """p = 1: <s_u> = sin 2b sin(2 g h_u) prod_{w != u} cos(2 g J_uw) for every u."""
+    h = np.asarray(h, dtype=np.float64)
+    n = h.shape[0]
+    Js = np.triu(np.asarray(J, dtype=np.float64).reshape(n, n), 1)
+    Js = Js + Js.T
+    out = np.empty(n)
+    for u in range(n):
+        others = [w for w in range(n) if w != u]
+        out[u] = np.sin(2 * beta) * np.sin(2 * gamma * h[u]) * np.prod(np.cos(2 * gamma * Js[u, others]))
+    return out
+
+
 def p1_expect_hc(h, J, gamma: float, beta: float) -> float:
     h = np.asarray(h, dtype=np.float64)
     n = h.shape[0]

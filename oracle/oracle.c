@@ -186,6 +186,19 @@ double oracle_norm2(int n, const double *psi) {
     return acc;
 }
 
+/* spin expectations <sigma^z_i> = sum_z |psi_z|^2 s_i(z) for i = 0..n-1
+ * ("spin expectation values during the time evolution"; Fig. 5) */
+void oracle_spin_expectations(int n, const double *psi, double *out) {
+    uint64_t dim = 1ull << n;
+    for (int i = 0; i < n; ++i) {
+        double acc = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : acc)
+        for (int64_t z = 0; z < (int64_t)dim; ++z)
+            acc += (psi[2 * z] * psi[2 * z] + psi[2 * z + 1] * psi[2 * z + 1]) * spin((uint64_t)z, i);
+        out[i] = acc;
+    }
+}
+
 /* success probability: sum over the listed ground states of |psi_z|^2 */
 double oracle_success_prob(int n, const double *psi, const uint64_t *gs, int count) {
     (void)n;

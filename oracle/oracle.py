@@ -61,6 +61,7 @@ def lib():
         L.oracle_ground_states.restype = ctypes.c_int
         L.oracle_ground_states.argtypes = [ctypes.c_int, _D, _D, _U64, ctypes.c_int, _D]
         L.oracle_num_threads.restype = ctypes.c_int
+        L.oracle_spin_expectations.argtypes = [ctypes.c_int, _D, _D]
         _lib = L
     return _lib
 
@@ -179,6 +180,14 @@ def ground_states(h, J, max_out: int = 64):
     cnt = lib().oracle_ground_states(n, _dp(h), _dp(J), out.ctypes.data_as(_U64), max_out,
                                      ctypes.byref(emin))
     return [int(x) for x in out[: min(cnt, max_out)]], emin.value, cnt
+
+
+def spin_expectations(psi: np.ndarray) -> np.ndarray:
+    """<sigma^z_i> = sum_z |psi_z|^2 s_i(z), i = 0..n-1."""
+    n = int(psi.shape[0]).bit_length() - 1
+    out = np.empty(n)
+    lib().oracle_spin_expectations(n, _dp(_psi_view(psi)), _dp(out))
+    return out
 
 
 def num_threads() -> int:

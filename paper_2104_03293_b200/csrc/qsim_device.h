@@ -89,12 +89,28 @@ struct GatherParams {
     unsigned char pos[NMAX];
 };
 
+struct EnumParams {
+    const double *h, *J;     // logical frame
+    int n;
+    u64 u0, u1;              // tile range (tile u = labels u*4096 .. u*4096+4095)
+    int collect;             // 0: per-CTA minimum into part; 1: collect labels with E == emin
+    double emin;
+    u64 *out;
+    unsigned long long *count;
+    int max_out;
+    double *part;
+};
+
 struct ProbeSet {
     int L[KT];
     int k;
     u64 lmask;
 };
 
+cudaError_t launch_spin(const PassParams &P, double *part, int grid, cudaStream_t s);
+cudaError_t launch_sum_vec(const double *part, int nparts, int n, double *out, cudaStream_t s);
+cudaError_t launch_enum(const EnumParams &E, int grid, cudaStream_t s);
+cudaError_t launch_min_partials(const double *part, int nparts, double *res, cudaStream_t s);
 size_t pass_smem_bytes();
 size_t tma_smem_bytes();
 cudaError_t setup_tma_kernels();

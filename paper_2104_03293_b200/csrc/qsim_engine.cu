@@ -263,6 +263,7 @@ struct qsim {
     int fr_slot = 0;
     bool fr_valid = false;     // d_fr[fr_slot] matches pos[]
     const double *cur_hp = nullptr, *cur_Jp = nullptr;
+    double *d_hlog = nullptr;  // logical-frame (h, J) for the enumeration kernel
     bool tilemajor = false;    // single GPU: out-of-place relabelling schedule (second buffer)
     TileSet tmset;             // its fixed tile shape: bits {0,1,2} + {12..20}
     double *d_part = nullptr, *d_res = nullptr, *d_ang = nullptr;
@@ -903,6 +904,7 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
         q->own_psi = true;
     }
     for (int k = 0; k < qsim::NFR; ++k) CK(cudaMalloc(&q->d_fr[k], sizeof(double) * ((size_t)n + (size_t)n * n)));
+    CK(cudaMalloc(&q->d_hlog, sizeof(double) * ((size_t)n + (size_t)n * n)));
     reset_perm(q);
     CK(cudaMalloc(&q->d_part, sizeof(double) * 2 * 4 * q->num_sms));
     CK(cudaMalloc(&q->d_res, sizeof(double) * 2));
@@ -1041,6 +1043,7 @@ int qsim_destroy(qsim_t *q) {
     if (q->tmp && q->tmp != q->user_buf) cudaFree(q->tmp);
     for (int k = 0; k < qsim::NFR; ++k)
         if (q->d_fr[k]) cudaFree(q->d_fr[k]);
+    if (q->d_hlog) cudaFree(q->d_hlog);
     if (q->d_part) cudaFree(q->d_part);
     if (q->d_res) cudaFree(q->d_res);
     if (q->d_ang) cudaFree(q->d_ang);
@@ -1068,6 +1071,12 @@ int qsim_set_ising(qsim_t *q, const double *h, const double *J) {
     }
     q->h = hh;
     q->J = JJ;
+    {
+        std::vector<double> lg((size_t)n + (size_t)n * n);
+        std::copy(hh.begin(), hh.end(), lg.begin());
+        std::copy(JJ.begin(), JJ.end(), lg.begin() + n);
+        CK(cudaMemcpyAsync(q->d_hlog, lg.data(), sizeof(double) * lg.size(), cudaMemcpyHostToDevice, q->st));
+    }
     q->fr_valid = false;
     int rc = ensure_frame(q);
     if (rc) return rc;
@@ -1202,6 +1211,177 @@ int qsim_energies(qsim_t *q, uint64_t first, uint64_t count, double *out) {
         CK(cudaStreamSynchronize(q->st));
     }
     return QSIM_OK;
+}
+
+int qsim_spin_expectations(qsim_t *q, double *out) {
+    if (!q) return QSIM_EINVAL;
+    if (!out) return fail(q, QSIM_EINVAL, "out is NULL");
+    if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
+    if (q->m <= qk::KT) {  // small states: amplitudes are few; gather and sum in the fixed order
+        const u64 dim = 1ull << q->n;
+        std::vector<double> amp(2 * dim);
+        int rc = gather_host(q, 0, dim, nullptr, amp.data());
+        if (rc) return rc;
+        for (int i = 0; i < q->n; ++i) {
+            double acc = 0.0;
+            for (u64 z = 0; z < dim; ++z)
+                acc += (amp[2 * z] * amp[2 * z] + amp[2 * z + 1] * amp[2 * z + 1]) * (((z >> i) & 1) ? 1.0 : -1.0);
+            out[i] = acc;
+        }
+        return QSIM_OK;
+    }
+    int rc = materialize_plus(q);
+    if (rc) return rc;
+    const TileSet &S = q->sets[0];
+    qk::PassParams P = base_params(q, S);
+    P.flip = q->flip;
+    const int grid = grid_for(q, S.ntiles);
+    rc = scratch(q, sizeof(double) * ((size_t)grid * q->n + q->n));
+    if (rc) return rc;
+    double *part = (double *)q->d_scratch, *vec = part + (size_t)grid * q->n;
+    CK(qk::launch_spin(P, part, grid, q->st));
+    CK(qk::launch_sum_vec(part, grid, q->n, vec, q->st));
+    q->launches += 2;
+    if (q->world > 1) NK(ncclAllReduce(vec, vec, q->n, ncclDouble, ncclSum, q->comm, q->st));
+    std::vector<double> phys(q->n);
+    CK(cudaMemcpyAsync(phys.data(), vec, sizeof(double) * q->n, cudaMemcpyDeviceToHost, q->st));
+    CK(cudaStreamSynchronize(q->st));
+    for (int a = 0; a < q->n; ++a) out[a] = phys[q->pos[a]];  // flips already folded in
+    return QSIM_OK;
+}
+
+int qsim_apply_aqa_traced(qsim_t *q, double T, int p, const double *s, const double *A, const double *B,
+                          int n_knots, double *trace) {
+    if (!q) return QSIM_EINVAL;
+    if (p < 2) return fail(q, QSIM_EINVAL, "AQA needs p >= 2 (s_k = (k-1)/(p-1))");
+    if (!trace) return fail(q, QSIM_EINVAL, "trace is NULL");
+    std::vector<double> g(p), b(p);
+    if (qsim_aqa_angles(T, p, s, A, B, n_knots, g.data(), b.data()) != QSIM_OK)
+        return fail(q, QSIM_EINVAL, "invalid schedule (knots must rise strictly from s=0 to s=1)");
+    for (int k = 0; k < p; ++k) {
+        int rc = qsim_apply_qaoa(q, &g[k], &b[k], 1);
+        if (rc) return rc;
+        rc = qsim_spin_expectations(q, trace + (size_t)k * q->n);
+        if (rc) return rc;
+    }
+    return QSIM_OK;
+}
+
+int qsim_ground_states(qsim_t *q, uint64_t *out, int max_out, double *emin_out, uint64_t *count_out) {
+    if (!q) return QSIM_EINVAL;
+    if (!emin_out || !count_out || max_out < 0 || (max_out > 0 && !out)) return fail(q, QSIM_EINVAL, "bad outputs");
+    if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
+    if (q->n < qk::KT) return fail(q, QSIM_EUNSUPPORTED, "enumeration needs n >= 12");
+    const u64 ntiles = 1ull << (q->n - qk::KT);
+    const u64 u0 = ntiles * (u64)q->rank / (u64)q->world, u1 = ntiles * (u64)(q->rank + 1) / (u64)q->world;
+    const int grid = (int)std::max<u64>(1, std::min<u64>((u64)q->num_sms * 8, u1 - u0));
+    const int cap = std::max(max_out, 1);
+    int rc = scratch(q, sizeof(double) * (grid + 1) + sizeof(unsigned long long) * 2 + sizeof(u64) * cap);
+    if (rc) return rc;
+    double *part = (double *)q->d_scratch, *res = part + grid;
+    unsigned long long *cnt = (unsigned long long *)(res + 1);
+    u64 *lst = (u64 *)(cnt + 2);
+    qk::EnumParams E{};
+    E.h = q->d_hlog;
+    E.J = q->d_hlog + q->n;
+    E.n = q->n;
+    E.u0 = u0;
+    E.u1 = u1;
+    E.part = part;
+    E.collect = 0;
+    CK(qk::launch_enum(E, grid, q->st));
+    CK(qk::launch_min_partials(part, grid, res, q->st));
+    q->launches += 2;
+    if (q->world > 1) NK(ncclAllReduce(res, res, 1, ncclDouble, ncclMin, q->comm, q->st));
+    double emin = 0.0;
+    CK(cudaMemcpyAsync(&emin, res, sizeof(double), cudaMemcpyDeviceToHost, q->st));
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), q->st));
+    CK(cudaStreamSynchronize(q->st));
+    E.collect = 1;
+    E.emin = emin;
+    E.out = lst;
+    E.count = cnt;
+    E.max_out = cap;
+    CK(qk::launch_enum(E, grid, q->st));
+    q->launches++;
+    unsigned long long c = 0;
+    CK(cudaMemcpyAsync(&c, cnt, sizeof(c), cudaMemcpyDeviceToHost, q->st));
+    CK(cudaStreamSynchronize(q->st));
+    std::vector<u64> mine((size_t)std::min<unsigned long long>(c, (unsigned long long)cap));
+    if (!mine.empty()) CK(cudaMemcpy(mine.data(), lst, sizeof(u64) * mine.size(), cudaMemcpyDeviceToHost));
+    std::sort(mine.begin(), mine.end());
+    std::vector<u64> all = mine;
+    unsigned long long total = c;
+    if (q->world > 1) {  // gather every rank's (count, first cap labels)
+        const size_t rec = 1 + (size_t)cap;
+        std::vector<u64> sendv(rec, ~0ull), recv(rec * q->world);
+        sendv[0] = c;
+        std::copy(mine.begin(), mine.end(), sendv.begin() + 1);
+        u64 *d = nullptr;
+        CK(cudaMalloc(&d, sizeof(u64) * rec * (1 + q->world)));
+        CK(cudaMemcpyAsync(d, sendv.data(), sizeof(u64) * rec, cudaMemcpyHostToDevice, q->st));
+        NK(ncclAllGather(d, d + rec, rec, ncclUint64, q->comm, q->st));
+        CK(cudaMemcpyAsync(recv.data(), d + rec, sizeof(u64) * rec * q->world, cudaMemcpyDeviceToHost, q->st));
+        CK(cudaStreamSynchronize(q->st));
+        cudaFree(d);
+        all.clear();
+        total = 0;
+        for (int r = 0; r < q->world; ++r) {
+            total += recv[r * rec];
+            for (size_t k = 0; k < (size_t)std::min<u64>(recv[r * rec], (u64)cap); ++k) all.push_back(recv[r * rec + 1 + k]);
+        }
+        std::sort(all.begin(), all.end());
+    }
+    for (int k = 0; k < max_out && k < (int)all.size(); ++k) out[k] = all[k];
+    *emin_out = emin;
+    *count_out = total;
+    return QSIM_OK;
+}
+
+int qsim_enumerate(int n, const double *h, const double *J, uint64_t *out, int max_out, double *emin_out,
+                   uint64_t *count_out, double *ms_out) {
+    if (n < qk::KT || n > 48 || !h || !J || !emin_out || !count_out || max_out < 0 || (max_out > 0 && !out))
+        return fail(nullptr, QSIM_EINVAL, "qsim_enumerate: bad arguments (12 <= n <= 48)");
+    qsim *q = new qsim();  // a state-less handle: frames and scratch only
+    q->n = n;
+    q->m = n;
+    int rc = QSIM_OK;
+    auto body = [&]() -> int {
+        CK(cudaGetDevice(&q->dev));
+        CK(cudaDeviceGetAttribute(&q->num_sms, cudaDevAttrMultiProcessorCount, q->dev));
+        CK(cudaStreamCreateWithFlags(&q->st, cudaStreamNonBlocking));
+        q->own_stream = true;
+        std::vector<double> lg((size_t)n + (size_t)n * n, 0.0);
+        for (int i = 0; i < n; ++i) {
+            if (!std::isfinite(h[i])) return fail(q, QSIM_EINVAL, "h contains NaN/Inf");
+            lg[i] = h[i];
+            for (int j = i + 1; j < n; ++j) {
+                const double v = J[(size_t)i * n + j];
+                if (!std::isfinite(v)) return fail(q, QSIM_EINVAL, "J contains NaN/Inf");
+                lg[n + (size_t)i * n + j] = lg[n + (size_t)j * n + i] = v;
+            }
+        }
+        CK(cudaMalloc(&q->d_hlog, sizeof(double) * lg.size()));
+        CK(cudaMemcpyAsync(q->d_hlog, lg.data(), sizeof(double) * lg.size(), cudaMemcpyHostToDevice, q->st));
+        q->has_ising = true;
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, q->st));
+        int r = qsim_ground_states(q, out, max_out, emin_out, count_out);
+        CK(cudaEventRecord(e1, q->st));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (ms_out) *ms_out = ms;
+        return r;
+    };
+    rc = body();
+    if (rc != QSIM_OK) g_create_error = q->err;
+    qsim_destroy(q);
+    return rc;
 }
 
 int qsim_sync(qsim_t *q) {

@@ -35,7 +35,8 @@ _ERRNAMES = {QSIM_EINVAL: "EINVAL", QSIM_ENOMEM: "ENOMEM", QSIM_ERANGE: "ERANGE"
 # every symbol include/qsim.h declares (tests check the library exports all of them)
 EXPORTS = ["qsim_create", "qsim_create_ex", "qsim_destroy", "qsim_set_ising", "qsim_init_plus",
            "qsim_apply_qaoa", "qsim_apply_aqa", "qsim_aqa_angles", "qsim_expect_hc", "qsim_norm2",
-           "qsim_success_prob", "qsim_get_amplitudes", "qsim_energies", "qsim_sync",
+           "qsim_success_prob", "qsim_get_amplitudes", "qsim_energies", "qsim_spin_expectations",
+           "qsim_apply_aqa_traced", "qsim_ground_states", "qsim_enumerate", "qsim_sync",
            "qsim_plan_counts", "qsim_plan_positions", "qsim_nccl_unique_id",
            "qsim_bench_pass", "qsim_profile_enable", "qsim_profile_read", "qsim_kernel_launches", "qsim_last_error",
            "qsim_version"]
@@ -71,6 +72,10 @@ lib.qsim_success_prob.argtypes = [_H, _U64, ctypes.c_int, _D]
 lib.qsim_get_amplitudes.argtypes = [_H, ctypes.c_uint64, ctypes.c_uint64, _D]
 lib.qsim_energies.argtypes = [_H, ctypes.c_uint64, ctypes.c_uint64, _D]
 lib.qsim_sync.argtypes = [_H]
+lib.qsim_spin_expectations.argtypes = [_H, _D]
+lib.qsim_apply_aqa_traced.argtypes = [_H, ctypes.c_double, ctypes.c_int, _D, _D, _D, ctypes.c_int, _D]
+lib.qsim_ground_states.argtypes = [_H, _U64, ctypes.c_int, _D, _U64]
+lib.qsim_enumerate.argtypes = [ctypes.c_int, _D, _D, _U64, ctypes.c_int, _D, _U64, _D]
 lib.qsim_plan_counts.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                  ctypes.POINTER(ctypes.c_int), _U64]
 lib.qsim_plan_positions.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
@@ -181,6 +186,42 @@ def qsim_energies(h, first: int, count: int) -> np.ndarray:
     out = np.empty(count, dtype=np.float64)
     _check(lib.qsim_energies(h, int(first), int(count), _dp(out)), h)
     return out
+
+
+def qsim_spin_expectations(h, n: int) -> np.ndarray:
+    out = np.empty(n)
+    _check(lib.qsim_spin_expectations(h, _dp(out)), h)
+    return out
+
+
+def qsim_apply_aqa_traced(h, n: int, T: float, p: int, s, A, B) -> np.ndarray:
+    s, A, B = _f64(s), _f64(A), _f64(B)
+    tr = np.empty((p, n))
+    _check(lib.qsim_apply_aqa_traced(h, float(T), int(p), _dp(s), _dp(A), _dp(B), int(s.shape[0]), _dp(tr)), h)
+    return tr
+
+
+def qsim_ground_states(h, max_out: int = 64):
+    """-> (list of minimisers (ascending), minimum energy, number of minimisers)"""
+    out = np.zeros(max(max_out, 1), dtype=np.uint64)
+    emin = ctypes.c_double()
+    cnt = ctypes.c_uint64()
+    _check(lib.qsim_ground_states(h, out.ctypes.data_as(_U64), int(max_out), ctypes.byref(emin),
+                                  ctypes.byref(cnt)), h)
+    return [int(x) for x in out[: min(cnt.value, max_out)]], emin.value, cnt.value
+
+
+def qsim_enumerate(hfield, J, max_out: int = 64):
+    """-> (minimisers ascending, minimum energy, number of minimisers, device ms); no state."""
+    hf = _f64(hfield)
+    n = hf.shape[0]
+    JJ = _f64(J).reshape(n, n)
+    out = np.zeros(max(max_out, 1), dtype=np.uint64)
+    emin, ms = ctypes.c_double(), ctypes.c_double()
+    cnt = ctypes.c_uint64()
+    _check(lib.qsim_enumerate(n, _dp(hf), _dp(JJ), out.ctypes.data_as(_U64), int(max_out), ctypes.byref(emin),
+                              ctypes.byref(cnt), ctypes.byref(ms)))
+    return [int(x) for x in out[: min(cnt.value, max_out)]], emin.value, cnt.value, ms.value
 
 
 def qsim_sync(h) -> None:
@@ -300,6 +341,15 @@ class QSim:
         if count is None:
             count = (1 << self.n) - first
         return qsim_energies(self.h, first, count)
+
+    def spins(self):
+        return qsim_spin_expectations(self.h, self.n)
+
+    def apply_aqa_traced(self, T, p, s, A, B):
+        return qsim_apply_aqa_traced(self.h, self.n, T, p, s, A, B)
+
+    def ground_states(self, max_out=64):
+        return qsim_ground_states(self.h, max_out)
 
     def sync(self):
         qsim_sync(self.h)

@@ -296,3 +296,74 @@ def test_full_size_energies_sampled(Q, big30):
     assert np.array_equal(e, o.energies(h, J, first, cnt))
     z_star = int(sum(int(x_star[i]) << i for i in range(n)))
     assert big30.energies(z_star, 1)[0] + C == 0.0
+
+
+# ------------------------------------------------------------------ NEXT-2: <sigma^z_i>
+@pytest.mark.parametrize("n,p", [(5, 3), (16, 3), (22, 2)])
+def test_spin_expectations(Q, n, p):
+    h, J = inst.random_ising(n, 500 + n)
+    g, b = rand_angles(p, 600 + n)
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        s.init_plus()
+        s.apply_qaoa(g, b)
+        sz = s.spins()
+    ref = o.spin_expectations(o.qaoa_state(h, J, g, b))
+    assert np.max(np.abs(sz - ref)) <= 1e-11
+
+
+def test_spin_trace_aqa(Q):
+    n, p = 17, 5
+    h, J = inst.random_ising(n, 77)
+    s_, A, B = inst.toy_schedule()
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        s.init_plus()
+        tr = s.apply_aqa_traced(2.5, p, s_, A, B)
+        psi = s.amplitudes()
+    g, b = o.aqa_angles(2.5, p, s_, A, B)
+    ref = o.init_plus(n)
+    for k in range(p):
+        o.apply_layers(h, J, g[k:k + 1], b[k:k + 1], ref)
+        assert np.max(np.abs(tr[k] - o.spin_expectations(ref))) <= 1e-11
+    assert_state_close(psi, ref)
+
+
+def test_full_size_spins_p1_closed_form(Q, big30):
+    n = 30
+    h, J = inst.random_ising(n, 35)
+    big30.set_ising(h, J)
+    big30.init_plus()
+    big30.apply_qaoa([0.29], [-0.61])
+    sz = big30.spins()
+    assert np.max(np.abs(sz - cf.p1_spins(h, J, 0.29, -0.61))) <= 1e-10
+
+
+# ------------------------------------------------------------------ NEXT-3: enumeration
+@pytest.mark.parametrize("n,kind", [(12, "2sat"), (16, "ising"), (20, "cover"), (21, "ising")])
+def test_ground_states_enumeration(Q, n, kind):
+    if kind == "2sat":
+        clauses, _ = inst.planted_2sat(n, seed=1)
+        h, J, C = op.two_sat_to_ising(n, clauses)
+    elif kind == "cover":
+        a, _ = inst.exact_cover(n, F=80, seed=3, planted_rows=5, weight=13)
+        h, J, C = op.exact_cover_to_ising(a)
+    else:
+        h, J = inst.random_ising(n, 900 + n)
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        gs, emin, cnt = s.ground_states(max_out=16)
+    rgs, remin, rcnt = o.ground_states(h, J, max_out=16)
+    assert emin == remin and cnt == rcnt and gs == rgs[: len(gs)]
+
+
+def test_ground_states_full_size_exact_cover(Q, big30):
+    """n = 30 exact-cover-shaped instance: the planted cover is a ground state (E + C = 0)."""
+    n = 30
+    a, x_star = inst.exact_cover(n, seed=0)
+    h, J, C = op.exact_cover_to_ising(a)
+    big30.set_ising(h, J)
+    gs, emin, cnt = big30.ground_states(max_out=8)
+    z_star = int(sum(int(x_star[i]) << i for i in range(n)))
+    assert emin + C == 0.0 and z_star in gs and cnt >= 1
+    assert o.energy(h, J, gs[0]) == emin

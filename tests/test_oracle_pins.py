@@ -378,3 +378,23 @@ def test_exact_cover_instance_shape_matches_paper_r():
         x = x_star
         assert op.exact_cover_objective(a, x) == 0.0
     assert 30.0 < np.mean(rs) < 45.0, rs
+
+
+# ----------------------------------------------------------------------------- spin expectations (NEXT-2)
+def test_spin_expectations_dense_and_closed_form():
+    n = 8
+    h, J = inst.random_ising(n, 23)
+    g, b = rand_angles(3, 23)
+    psi = o.qaoa_state(h, J, g, b)
+    sz = o.spin_expectations(psi)
+    # dense <psi| sigma^z_i |psi> with sigma^z_i = diag(s_i(z)), |1> <-> +1
+    z = np.arange(1 << n)
+    for i in range(n):
+        si = np.where((z >> i) & 1, 1.0, -1.0)
+        assert abs(sz[i] - np.vdot(psi, si * psi).real) < 1e-14
+    # p = 1 closed form, and the n = 1 case of P2
+    for n2, seed in [(1, 0), (5, 1), (11, 2)]:
+        h2, J2 = inst.random_ising(n2, seed)
+        psi1 = o.qaoa_state(h2, J2, [0.41], [-0.83])
+        assert np.max(np.abs(o.spin_expectations(psi1) - cf.p1_spins(h2, J2, 0.41, -0.83))) < 1e-13
+    assert abs(cf.p1_spins([0.5], [[0.0]], 0.41, -0.83)[0] - cf.n1_spin(0.5, 0.41, -0.83)) < 1e-15

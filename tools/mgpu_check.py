@@ -81,6 +81,19 @@ for n in a.qubits:
         ref2 = o.qaoa_state(h, J, np.concatenate([g, g[:1]]), np.concatenate([b, b[:1]]))
         d2 = np.max(np.abs(psi2 - ref2))
         report(f"n={n} continued apply", d2 <= 1e-10, f"max|d|={d2:.2e}")
+    # 1a) spins (NEXT-2) and enumeration (NEXT-3) on the sharded handle
+    sim = Q.QSim(n, rank=rank, world=world, nccl_unique_id=new_uid())
+    sim.set_ising(h, J)
+    sim.init_plus()
+    sim.apply_qaoa(g, b)
+    sz = sim.spins()
+    gs, emin, cnt = sim.ground_states(max_out=8)
+    sim.close()
+    if rank == 0 and n <= 24:
+        ref = o.qaoa_state(h, J, g, b)
+        report(f"n={n} spins", np.max(np.abs(sz - o.spin_expectations(ref))) <= 1e-11)
+        rgs, remin, rcnt = o.ground_states(h, J, max_out=8)
+        report(f"n={n} ground states", emin == remin and cnt == rcnt and gs == rgs[: len(gs)])
     # 1b) p = 1 closed-form <H_C> (pin P4), any n
     sim = Q.QSim(n, rank=rank, world=world, nccl_unique_id=new_uid())
     sim.set_ising(h, J)
