@@ -61,6 +61,7 @@ struct PassParams {
     double2 *dst[8];
     int dbg;             // diagnostics (qsim_bench_pass): bit 0 skip stores, bit 1 skip state loads
     int tma_store;       // store tiles with TMA from the stage instead of STG from registers
+    int l2hint;          // L2 cache policy: bits 0-1 loads, bits 2-3 stores (0 none, 1 evict_first, 2 evict_last)
     // out-of-place tile-major store (single-GPU relabelling schedule): tile u goes to the
     // contiguous block out + (out_u << 12), out_u = sum_s ((u >> src_s) & (2^len_s - 1)) << dst_s
     int tmo;

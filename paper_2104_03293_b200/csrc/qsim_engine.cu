@@ -279,6 +279,7 @@ struct qsim {
     int use_tma = 1;           // TMA-pipelined pass kernel (QSIM_KERNEL=v4 selects the register-direct one)
     int l2promo = (int)CU_TENSOR_MAP_L2_PROMOTION_L2_128B;  // TMA L2 sector promotion (QSIM_L2PROMO=0..3)
     int tma_store = 1;         // TMA stores from the stage (QSIM_TMA_STORE=0: STG from registers)
+    int l2hint = 0;            // TMA L2 cache policy (QSIM_L2HINT, see PassParams::l2hint)
     std::string err;
     // optional per-pass timing (CUDA events on the handle's stream around each pass launch)
     bool prof = false;
@@ -404,6 +405,7 @@ qk::PassParams base_params(qsim *q, const TileSet &S) {
     // every tile touches up to 512 distinct 2 MiB pages and prefetching slows them (measured)
     P.prefetch = q->prefetch && S.full12;
     P.tma_store = q->tma_store;
+    P.l2hint = q->l2hint;
     return P;
 }
 
@@ -991,6 +993,7 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     if (const char *e = std::getenv("QSIM_PREFETCH")) q->prefetch = std::atoi(e);
     if (const char *e = std::getenv("QSIM_L2PROMO")) q->l2promo = std::atoi(e);
     if (const char *e = std::getenv("QSIM_TMA_STORE")) q->tma_store = std::atoi(e);
+    if (const char *e = std::getenv("QSIM_L2HINT")) q->l2hint = std::atoi(e);
     if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
     if (q->use_tma) {
         CK(qk::setup_tma_kernels());

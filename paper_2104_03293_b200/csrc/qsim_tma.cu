@@ -52,7 +52,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *tm, const int (&c)[5], uint64_t *bar) {
+// L2 cache policy for the streamed state (QSIM_L2HINT: 0 none, 1 evict_first, 2 evict_last)
+__device__ __forceinline__ uint64_t l2_policy(int kind) {
+    uint64_t pol = 0;
+    if (kind == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *tm, const int (&c)[5], uint64_t *bar,
+                                            int hint = 0) {
+    if (hint) {
+        const uint64_t pol = l2_policy(hint);
+        asm volatile(
+            "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(dst)),
+            "l"(reinterpret_cast<uint64_t>(tm)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]),
+            "r"(smem_u32(bar)), "l"(pol)
+            : "memory");
+        return;
+    }
     asm volatile(
         "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
@@ -67,12 +85,22 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
         "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ void tma_store_5d(const CUtensorMap *tm, const int (&c)[5], const void *src) {
-    asm volatile(
-        "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
-            reinterpret_cast<uint64_t>(tm)),
-        "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(src))
-        : "memory");
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap *tm, const int (&c)[5], const void *src,
+                                             int hint = 0) {
+    if (hint) {
+        const uint64_t pol = l2_policy(hint);
+        asm volatile(
+            "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4, %5}], [%6], %7;" ::
+                "l"(reinterpret_cast<uint64_t>(tm)),
+            "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(src)), "l"(pol)
+            : "memory");
+    } else {
+        asm volatile(
+            "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                reinterpret_cast<uint64_t>(tm)),
+            "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(src))
+            : "memory");
+    }
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
@@ -125,7 +153,7 @@ __device__ __forceinline__ void issue_tile(const PassParams &P, const TmaIssue &
 #pragma unroll
         for (int d = 0; d < 5; ++d)
             c[d] = P.tm_clen[d] ? (int)((ut >> P.tm_cshift[d]) & ((1ull << P.tm_clen[d]) - 1ull)) : 0;
-        tma_load_5d(I.stages + (size_t)s * TILE, I.tm, c, &I.full[s]);
+        tma_load_5d(I.stages + (size_t)s * TILE, I.tm, c, &I.full[s], P.l2hint & 3);
     }
     if (load_rec) bulk_load(I.srec + s, I.grec + ut, (uint32_t)TILE_REC_BYTES, &I.full[s]);
     __threadfence_block();
@@ -310,7 +338,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 if (gt == 0) {
                     int c[5];
                     tile_coords(P, ut, c);
-                    tma_store_5d(I.tm, c, sm);
+                    tma_store_5d(I.tm, c, sm, (P.l2hint >> 2) & 3);
                     bulk_wait_read0();
                     if (i + NSTAGE < ntl) issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
                 }
@@ -338,7 +366,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 if (gt == 0) {
                     int c[5];
                     tile_coords(P, ut, c);
-                    tma_store_5d(I.tm, c, sm);
+                    tma_store_5d(I.tm, c, sm, (P.l2hint >> 2) & 3);
                     bulk_wait_read0();
                     if (i + NSTAGE < ntl) issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
                 }
