@@ -159,6 +159,58 @@ int oracle_aqa_angles(double T, int p, const double *ks, const double *A, const 
     return 0;
 }
 
+/* QSDS "combined" second-order step, eq. AQA4, applied for l = 0..nsteps:
+ *   exp[i tau/2 sum_i (ht^x sigma^x_i + ht^z_i sigma^z_i)] exp[i tau sum_{i<j} Jt_ij s_i s_j]
+ *   exp[i tau/2 sum_i (...)]  with ht^x = A(s_l), ht^z_i = -B(s_l) h_i, Jt_ij = -B(s_l) J_ij
+ * (AQA0-AQA3), s_l = l tau / t_anneal, t_anneal = (nsteps+1) tau.
+ * Each single-spin exponential exactly: exp[i(a X + b Z)] = cos w I + i sin w / w (a X + b Z),
+ * w = sqrt(a^2 + b^2); sigma^z = diag(-1, +1) on (|0>, |1>).  psi is updated in place
+ * (the caller supplies |+>^n for Psi(0)). */
+static void qsds_half(int n, const double *h, double a_coef, double b_scale, double *psi) {
+    uint64_t dim = 1ull << n;
+    for (int q = 0; q < n; ++q) {
+        double a = a_coef, b = b_scale * h[q];
+        double w = sqrt(a * a + b * b);
+        double c = cos(w), sw = (w > 0.0) ? sin(w) / w : 1.0;
+        /* U = [[c - i sw b, i sw a], [i sw a, c + i sw b]] on (|0>, |1>) */
+        double u00r = c, u00i = -sw * b, u01r = 0.0, u01i = sw * a;
+        double u11r = c, u11i = sw * b;
+        uint64_t bit = 1ull << q;
+#pragma omp parallel for schedule(static)
+        for (int64_t z = 0; z < (int64_t)dim; ++z) {
+            if ((uint64_t)z & bit) continue;
+            uint64_t z1 = (uint64_t)z | bit;
+            double ar = psi[2 * z], ai = psi[2 * z + 1], br = psi[2 * z1], bi = psi[2 * z1 + 1];
+            psi[2 * z] = u00r * ar - u00i * ai + u01r * br - u01i * bi;
+            psi[2 * z + 1] = u00r * ai + u00i * ar + u01r * bi + u01i * br;
+            psi[2 * z1] = u01r * ar - u01i * ai + u11r * br - u11i * bi;
+            psi[2 * z1 + 1] = u01r * ai + u01i * ar + u11r * bi + u11i * br;
+        }
+    }
+}
+
+void oracle_apply_qsds(int n, const double *h, const double *J, double tau, int nsteps, const double *ks,
+                       const double *A, const double *B, int m, double *psi) {
+    uint64_t dim = 1ull << n;
+    double *zeros = (double *)calloc((size_t)n, sizeof(double));
+    for (int l = 0; l <= nsteps; ++l) {
+        double sl = (double)l / (double)(nsteps + 1);
+        double Al = pwl(ks, A, m, sl), Bl = pwl(ks, B, m, sl);
+        qsds_half(n, h, 0.5 * tau * Al, -0.5 * tau * Bl, psi);
+        /* exp[i tau sum Jt s s] = exp[-i tau B E_J(z)], E_J = sum_{i<j} J_ij s_i s_j */
+#pragma omp parallel for schedule(static)
+        for (int64_t z = 0; z < (int64_t)dim; ++z) {
+            double e = oracle_energy(n, zeros, J, (uint64_t)z);
+            double th = tau * Bl * e, c = cos(th), s = sin(th);
+            double re = psi[2 * z], im = psi[2 * z + 1];
+            psi[2 * z] = c * re + s * im;
+            psi[2 * z + 1] = c * im - s * re;
+        }
+        qsds_half(n, h, 0.5 * tau * Al, -0.5 * tau * Bl, psi);
+    }
+    free(zeros);
+}
+
 /* <H_C> = sum_z |psi_z|^2 E(z)  (E_p(beta,gamma)), constant C excluded (R4).
  * Also returns sum_z |psi_z|^2 |E(z)| in *abs_out (tolerance scale, reading R12). */
 double oracle_expect_hc(int n, const double *h, const double *J, const double *psi,

@@ -62,6 +62,8 @@ def lib():
         L.oracle_ground_states.argtypes = [ctypes.c_int, _D, _D, _U64, ctypes.c_int, _D]
         L.oracle_num_threads.restype = ctypes.c_int
         L.oracle_spin_expectations.argtypes = [ctypes.c_int, _D, _D]
+        L.oracle_apply_qsds.argtypes = [ctypes.c_int, _D, _D, ctypes.c_double, ctypes.c_int, _D, _D, _D,
+                                        ctypes.c_int, _D]
         _lib = L
     return _lib
 
@@ -188,6 +190,16 @@ def spin_expectations(psi: np.ndarray) -> np.ndarray:
     out = np.empty(n)
     lib().oracle_spin_expectations(n, _dp(_psi_view(psi)), _dp(out))
     return out
+
+
+def qsds_state(h, J, tau: float, nsteps: int, s, A, B) -> np.ndarray:
+    """QSDS combined second-order stepping (eq. AQA4) from |+>^n, l = 0..nsteps."""
+    n, h, J = _hJ(h, J)
+    s, A, B = _f64(s), _f64(A), _f64(B)
+    psi = init_plus(n)
+    lib().oracle_apply_qsds(n, _dp(h), _dp(J), float(tau), int(nsteps), _dp(s), _dp(A), _dp(B), s.shape[0],
+                            _dp(_psi_view(psi)))
+    return psi
 
 
 def num_threads() -> int:

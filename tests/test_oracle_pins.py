@@ -398,3 +398,67 @@ def test_spin_expectations_dense_and_closed_form():
         psi1 = o.qaoa_state(h2, J2, [0.41], [-0.83])
         assert np.max(np.abs(o.spin_expectations(psi1) - cf.p1_spins(h2, J2, 0.41, -0.83))) < 1e-13
     assert abs(cf.p1_spins([0.5], [[0.0]], 0.41, -0.83)[0] - cf.n1_spin(0.5, 0.41, -0.83)) < 1e-15
+
+
+# ----------------------------------------------------------------------------- QSDS combined step (NEXT-1)
+def _dense_Z(n):
+    z = np.arange(1 << n)
+    return [np.where((z >> q) & 1, 1.0, -1.0) for q in range(n)]  # sigma^z_q = diag(s_q)
+
+
+def test_qsds_matches_dense_exponentials():
+    """Each factor of eq. AQA4 as a dense expm of its generator (AQA0-AQA3), n <= 5."""
+    n, nsteps, tau = 5, 3, 0.37
+    h, J = inst.random_ising(n, 31)
+    s_, A, B = inst.dw_like_schedule()
+    A, B = 0.3 * A, 0.3 * B
+    HD = dense_HD(n)
+    Zs = _dense_Z(n)
+    EJ = dense_energies(np.zeros(n), J)
+    psi = np.full(1 << n, 2.0 ** (-n / 2), dtype=complex)
+    for l in range(nsteps + 1):
+        sl = l / (nsteps + 1)
+        Al, Bl = np.interp(sl, s_, A), np.interp(sl, s_, B)
+        gen = Al * HD + np.diag(sum(-Bl * h[q] * Zs[q] for q in range(n)))  # sum_alpha ht^alpha sigma^alpha
+        half = sla.expm(1j * tau / 2 * gen)
+        psi = half @ (np.exp(-1j * tau * Bl * EJ) * (half @ psi))
+    got = o.qsds_state(h, J, tau, nsteps, s_, A, B)
+    assert np.max(np.abs(got - psi)) < 1e-13
+
+
+def test_qsds_trivial_problem():
+    n, nsteps, tau = 6, 4, 0.5
+    s_, A, B = inst.toy_schedule()
+    got = o.qsds_state(np.zeros(n), np.zeros((n, n)), tau, nsteps, s_, A, B)
+    phase = sum(tau * np.interp(l / (nsteps + 1), s_, A) for l in range(nsteps + 1))
+    assert np.max(np.abs(got - np.exp(1j * n * phase) * 2.0 ** (-n / 2))) < 1e-14
+
+
+def test_qsds_first_order_convergence_and_forms_agree():
+    """QSDS (left-endpoint s_l = l/(n+1)) converges to the TDSE of H(s) = A(s) H_I + B(s) H_C at
+    first order (reading R9); the split (AQA) and combined (QSDS) forms approach each other."""
+    n = 4
+    h, J = inst.random_ising(n, 41)
+    sA, A, B = np.array([0.0, 1.0]), np.array([1.0, 0.0]), np.array([0.0, 1.0])
+    T = 3.0
+    E = dense_energies(h, J)
+    HD = dense_HD(n)
+
+    def rhs(t, y):
+        s = t / T
+        return -1j * (((1 - s) * (-HD) + s * np.diag(E)) @ y)
+
+    y0 = np.full(1 << n, 2.0 ** (-n / 2), dtype=complex)
+    ref = solve_ivp(rhs, (0, T), y0, method="DOP853", rtol=1e-12, atol=1e-13).y[:, -1]
+    errs, mutual = [], []
+    for steps in [16, 32, 64, 128]:
+        tau = T / steps
+        psi = o.qsds_state(h, J, tau, steps - 1, sA, A, B)
+        ov = np.vdot(ref, psi)
+        errs.append(np.linalg.norm(psi - ov / abs(ov) * ref))
+        aqa = o.aqa_state(h, J, T, steps, sA, A, B)
+        ov2 = np.vdot(aqa, psi)
+        mutual.append(np.linalg.norm(psi - ov2 / abs(ov2) * aqa))
+    ratios = [errs[i] / errs[i + 1] for i in range(3)]
+    assert all(1.7 <= r <= 2.3 for r in ratios), ratios
+    assert all(mutual[i + 1] < mutual[i] for i in range(3)), mutual
