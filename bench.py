@@ -197,7 +197,10 @@ def main():
         obj = [Q.qsim_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: the library enqueues every kernel on it and the timing events are
+    # recorded on it (torch's default stream is the legacy null stream, handle 0)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sim = Q.QSim(n, rank=rank, world=world, nccl_unique_id=uid, cuda_stream=stream.cuda_stream)
     sim.set_ising(w["h"], w["J"])
 

@@ -107,6 +107,17 @@ int qsim_apply_qaoa(qsim_t *q, const double *gamma, const double *beta, int p);
 int qsim_apply_aqa(qsim_t *q, double T, int p, const double *s, const double *A, const double *B,
                    int n_knots);
 
+/* the QSDS "combined" second-order Suzuki-Trotter stepping of eq. AQA4
+ * applied to the current state for l = 0..n_steps:
+ *   exp[i tau/2 sum_i (A sigma^x_i - B h_i sigma^z_i)] exp[-i tau B sum_{i<j} J_ij s_i s_j]
+ *   exp[i tau/2 sum_i (A sigma^x_i - B h_i sigma^z_i)],  A, B at s_l = l / (n_steps + 1)
+ * (AQA0-AQA3: h~x = A, h~z_i = -B h_i, J~z = -B J; t_anneal = (n_steps + 1) tau), each
+ * single-spin exponential exact.  Consecutive half-steps are merged into one per-qubit
+ * 2x2 unitary, so n_steps + 2 general-mixer layers run on the tile-pass kernels.  A, B in
+ * angular units per unit of tau. */
+int qsim_apply_qsds(qsim_t *q, double tau, int n_steps, const double *s, const double *A, const double *B,
+                    int n_knots);
+
 /* Host-only helper (no device work): the angles qsim_apply_aqa uses. */
 int qsim_aqa_angles(double T, int p, const double *s, const double *A, const double *B,
                     int n_knots, double *gamma_out, double *beta_out);

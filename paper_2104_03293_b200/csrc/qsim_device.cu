@@ -236,6 +236,18 @@ __global__ void __launch_bounds__(512) small_kernel(const SmallParams P) {
         sincos(b, &sb, &cb);
         for (int q = 0; q < n; ++q) {
             __syncthreads();
+            if (P.gmat) {  // general per-qubit 2x2 (QSDS combined step)
+                const double2 *M = P.gmat + ((size_t)k * n + q) * 4;
+                const double2 m00 = M[0], m01 = M[1], m10 = M[2], m11 = M[3];
+                for (int r = tid; r < dim / 2; r += nt) {
+                    const int z0 = ((r >> q) << (q + 1)) | (r & ((1 << q) - 1));
+                    const int z1 = z0 | (1 << q);
+                    const double2 a = st[z0], bb = st[z1];
+                    st[z0] = cmac(m00, a, cmac(m01, bb, make_double2(0.0, 0.0)));
+                    st[z1] = cmac(m10, a, cmac(m11, bb, make_double2(0.0, 0.0)));
+                }
+                continue;
+            }
             for (int r = tid; r < dim / 2; r += nt) {
                 const int z0 = ((r >> q) << (q + 1)) | (r & ((1 << q) - 1));
                 const int z1 = z0 | (1 << q);

@@ -64,6 +64,10 @@ struct PassParams {
     int l2hint;          // L2 cache policy: bits 0-1 loads, bits 2-3 stores (0 none, 1 evict_first, 2 evict_last)
     // out-of-place tile-major store (single-GPU relabelling schedule): tile u goes to the
     // contiguous block out + (out_u << 12), out_u = sum_s ((u >> src_s) & (2^len_s - 1)) << dst_s
+    // general mixer (QSDS combined step, NEXT-1): per tile bit a 2x2 complex matrix
+    // {m00, m01, m10, m11} acting on (|0>, |1>) instead of the scaled R_x butterfly
+    int gmix;
+    double2 gm1[KT][4], gm2[KT][4];
     int tmo;
     double2 *out;
     int onseg;
@@ -76,6 +80,7 @@ struct SmallParams {
     double2 *psi;
     const double *hp, *Jp;
     const double *ang;   // gamma[p], beta[p]
+    const double2 *gmat; // optional general mixers: [p][n][4] (then beta is unused)
     int n, p, init, reduce;
     double a0;
     double *res;         // 2 doubles

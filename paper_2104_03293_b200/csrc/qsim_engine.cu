@@ -53,6 +53,7 @@ struct PassOp {
     double b1, b2, gamma;
     bool swap_after;  // multi-GPU: global-qubit swap (NCCL, in place) after this pass
     bool swap_fused;  // multi-GPU: this pass stores its output swapped into the peers' buffers
+    int l1 = 0, l2 = 0;  // layer indices of mix1 / mix2 (general-mixer mode)
 };
 
 TileSet make_set(int m, const std::vector<int> &Lpos, unsigned own) {
@@ -165,14 +166,14 @@ std::vector<PassOp> build_schedule(int nsets, int g, int p, const double *gam, c
         if (P > 1) order.push_back(0);
         for (int i = 2; i < P; ++i) order.push_back(i);
         auto seq = [&](int k, int idx) { return order[(k % 2 == 0) ? idx : P - 1 - idx]; };
-        ops.push_back({seq(0, 0), first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false, false});
+        ops.push_back({seq(0, 0), first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false, false, 0, 0});
         for (int k = 0; k < p; ++k) {
             for (int idx = 1; idx < P; ++idx) {
                 int s = seq(k, idx);
                 if (idx == P - 1 && k < p - 1)
-                    ops.push_back({s, false, true, false, ~0u, ~0u, bet[k], bet[k + 1], gam[k + 1], false, false});
+                    ops.push_back({s, false, true, false, ~0u, ~0u, bet[k], bet[k + 1], gam[k + 1], false, false, k, k + 1});
                 else
-                    ops.push_back({s, false, false, false, ~0u, 0u, bet[k], 0.0, 0.0, false, false});
+                    ops.push_back({s, false, false, false, ~0u, 0u, bet[k], 0.0, 0.0, false, false, k, 0});
             }
         }
     } else {
@@ -186,14 +187,14 @@ std::vector<PassOp> build_schedule(int nsets, int g, int p, const double *gam, c
         const unsigned arrivals = ((1u << g) - 1) << (qk::KT - g);  // top g tile bits of the top set
         for (int k = 0; k < p; ++k) {
             if (k == 0)
-                ops.push_back({top, first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false, fused});
+                ops.push_back({top, first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false, fused, 0, 0});
             else
-                ops.push_back({top, false, true, false, arrivals, ~0u, bet[k - 1], bet[k], gam[k], false, fused});
+                ops.push_back({top, false, true, false, arrivals, ~0u, bet[k - 1], bet[k], gam[k], false, fused, k - 1, k});
             for (int s = P - 2; s >= 0; --s)
-                ops.push_back({s, false, false, false, ~0u, 0u, bet[k], 0.0, 0.0, false, false});
+                ops.push_back({s, false, false, false, ~0u, 0u, bet[k], 0.0, 0.0, false, false, k, 0});
             if (!fused) ops.back().swap_after = true;
         }
-        ops.push_back({top, false, false, false, arrivals, 0u, bet[p - 1], 0.0, 0.0, false, false});
+        ops.push_back({top, false, false, false, arrivals, 0u, bet[p - 1], 0.0, 0.0, false, false, p - 1, 0});
     }
     ops.back().reduce = true;
     return ops;
@@ -264,6 +265,11 @@ struct qsim {
     bool fr_valid = false;     // d_fr[fr_slot] matches pos[]
     const double *cur_hp = nullptr, *cur_Jp = nullptr;
     double *d_hlog = nullptr;  // logical-frame (h, J) for the enumeration kernel
+    // general-mixer mode (QSDS combined step): per layer, per logical qubit a 2x2 matrix; the
+    // phase uses the J-only frame (frame_noh)
+    const std::vector<double2> *gmats = nullptr;  // [layer][qubit][4]
+    bool frame_noh = false;
+    bool fr_noh_built = false;
     bool tilemajor = false;    // single GPU: out-of-place relabelling schedule (second buffer)
     TileSet tmset;             // its fixed tile shape: bits {0,1,2} + {12..20}
     double *d_part = nullptr, *d_res = nullptr, *d_ang = nullptr;
@@ -344,12 +350,12 @@ void relabel(qsim *q, const int *newp) {
 // make cur_hp / cur_Jp the physical-frame copy of (h, J) for the current permutation
 // (stream-ordered upload into the next ring slot; older slots stay valid for queued kernels)
 int ensure_frame(qsim *q) {
-    if (q->fr_valid) return QSIM_OK;
+    if (q->fr_valid && q->fr_noh_built == q->frame_noh) return QSIM_OK;
     const int n = q->n;
     std::vector<double> fr((size_t)n + (size_t)n * n, 0.0);
     for (int a = 0; a < n; ++a) {
         const int pa = q->pos[a];
-        fr[pa] = q->h[a];
+        fr[pa] = q->frame_noh ? 0.0 : q->h[a];
         for (int b = 0; b < n; ++b) fr[n + (size_t)pa * n + q->pos[b]] = q->J[(size_t)a * n + b];
     }
     const int slot = (q->fr_slot + 1) % qsim::NFR;
@@ -358,6 +364,7 @@ int ensure_frame(qsim *q) {
     q->cur_hp = q->d_fr[slot];
     q->cur_Jp = q->d_fr[slot] + n;
     q->fr_valid = true;
+    q->fr_noh_built = q->frame_noh;
     return QSIM_OK;
 }
 
@@ -533,6 +540,27 @@ int prof_events(qsim *q, cudaEvent_t *a, cudaEvent_t *b) {
     return QSIM_OK;
 }
 
+// general-mixer mode: per tile bit the 2x2 matrix of the qubit sitting there, for the layers
+// of mix1 / mix2; no scaled-butterfly scalar and no X-gate flips
+void set_gmix(const qsim *q, qk::PassParams &P, const int *L, const PassOp &op) {
+    if (!q->gmats) return;
+    const std::vector<double2> &G = *q->gmats;
+    P.gmix = 1;
+    P.c1.form = P.c2.form = 0;
+    P.c1.t = P.c2.t = 0.0;
+    P.scale = make_double2(1.0, 0.0);
+    for (int t = 0; t < qk::KT; ++t) {
+        const int a = q->qat[L[t]];
+        // a flipped position stores the logical |1> amplitude in its 0 slot: use X M X
+        const bool fl = (q->flip >> L[t]) & 1ull;
+        for (int e = 0; e < 4; ++e) {
+            const int es = fl ? 3 - e : e;
+            P.gm1[t][e] = G[((size_t)op.l1 * q->n + a) * 4 + es];
+            P.gm2[t][e] = G[((size_t)op.l2 * q->n + a) * 4 + es];
+        }
+    }
+}
+
 int apply_tilemajor(qsim *q, const double *gam, const double *bet, int p);
 
 int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
@@ -561,7 +589,15 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         S.n = q->n;
         S.p = p;
         S.init = q->pending_plus ? 1 : 0;
-        S.reduce = 1;
+        S.reduce = q->gmats ? 0 : 1;
+        S.gmat = nullptr;
+        if (q->gmats) {
+            const std::vector<double2> &G = *q->gmats;
+            int rc = scratch(q, sizeof(double2) * G.size());
+            if (rc) return rc;
+            CK(cudaMemcpyAsync(q->d_scratch, G.data(), sizeof(double2) * G.size(), cudaMemcpyHostToDevice, q->st));
+            S.gmat = (const double2 *)q->d_scratch;
+        }
         S.a0 = std::pow(2.0, -0.5 * q->n);
         S.res = q->d_res;
         CK(qk::launch_small(S, q->st));
@@ -569,7 +605,7 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         // the host copy of the angles must outlive the async copy
         CK(cudaStreamSynchronize(q->st));
         q->pending_plus = false;
-        q->res_valid = true;
+        q->res_valid = !q->gmats;
         return QSIM_OK;
     }
     std::vector<PassOp> ops = build_schedule((int)q->sets.size(), q->g, p, gam, bet, q->pending_plus, q->fused_swap);
@@ -589,6 +625,7 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         P.mix2 = op.phase ? m2 : 0u;
         std::complex<double> sc = cpow_int(k1, __builtin_popcount(P.mix1)) * cpow_int(k2, __builtin_popcount(P.mix2));
         P.scale = make_double2(sc.real(), sc.imag());
+        set_gmix(q, P, S.L, op);
         // X gates of the |tan beta| > 1 form -> flip mask (energies of this pass use the
         // mask after mix1; the state after the pass carries the mask after mix2)
         auto posmask = [&](unsigned tm) {
@@ -644,6 +681,7 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         }
     }
     q->pending_plus = false;
+    if (q->gmats) return QSIM_OK;  // J-only frame: <H_C> is recomputed on demand
     return finish_reduce(q, last_grid);
 }
 
@@ -747,6 +785,7 @@ int apply_tilemajor(qsim *q, const double *gam, const double *bet, int p) {
         P.mix2 = op.phase ? (op.mix2 & own) : 0u;
         std::complex<double> sc = cpow_int(k1, __builtin_popcount(P.mix1)) * cpow_int(k2, __builtin_popcount(P.mix2));
         P.scale = make_double2(sc.real(), sc.imag());
+        set_gmix(q, P, S.L, op);
         auto posmask = [&](unsigned tm) {
             u64 r = 0;
             for (int t = 0; t < qk::KT; ++t)
@@ -787,6 +826,7 @@ int apply_tilemajor(qsim *q, const double *gam, const double *bet, int p) {
         q->tmp = q->bufs[q->cur ^ 1];
     }
     q->pending_plus = false;
+    if (q->gmats) return QSIM_OK;  // J-only frame: <H_C> is recomputed on demand
     return finish_reduce(q, last_grid);
 }
 
@@ -1134,6 +1174,63 @@ int qsim_apply_aqa(qsim_t *q, double T, int p, const double *s, const double *A,
     if (qsim_aqa_angles(T, p, s, A, B, n_knots, g.data(), b.data()) != QSIM_OK)
         return fail(q, QSIM_EINVAL, "invalid schedule (knots must rise strictly from s=0 to s=1)");
     return qsim_apply_qaoa(q, g.data(), b.data(), p);
+}
+
+int qsim_apply_qsds(qsim_t *q, double tau, int n_steps, const double *s, const double *A, const double *B,
+                    int n_knots) {
+    if (!q) return QSIM_EINVAL;
+    if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
+    if (n_steps < 0 || !s || !A || !B || n_knots < 2 || !std::isfinite(tau))
+        return fail(q, QSIM_EINVAL, "need tau, n_steps >= 0 and a schedule");
+    for (int j = 0; j < n_knots; ++j) {
+        if (!std::isfinite(s[j]) || !std::isfinite(A[j]) || !std::isfinite(B[j])) return fail(q, QSIM_EINVAL, "NaN in schedule");
+        if (j > 0 && !(s[j] > s[j - 1])) return fail(q, QSIM_EINVAL, "knots must rise strictly");
+    }
+    if (s[0] != 0.0 || s[n_knots - 1] != 1.0) return fail(q, QSIM_EINVAL, "knots must span [0, 1]");
+    if (!q->use_tma && q->m > qk::KT) return fail(q, QSIM_EUNSUPPORTED, "QSDS needs the TMA pass kernel");
+    const int n = q->n, L = n_steps + 1;  // step operators l = 0..n_steps (eq. AQA4)
+    // exact half-step exp[i tau/2 (A X - B h_q Z)] per qubit (AQA3), Z = diag(-1, +1)
+    auto half = [&](int l, int a, std::complex<double> (&U)[4]) {
+        const double sl = (double)l / (double)L;
+        const double al = 0.5 * tau * pwl(s, A, n_knots, sl), bl = -0.5 * tau * pwl(s, B, n_knots, sl) * q->h[a];
+        const double w = std::sqrt(al * al + bl * bl), c = std::cos(w), sw = w > 0.0 ? std::sin(w) / w : 1.0;
+        U[0] = {c, -sw * bl};
+        U[1] = {0.0, sw * al};
+        U[2] = {0.0, sw * al};
+        U[3] = {c, sw * bl};
+    };
+    // layers k = 0..L: mixer M_k (k = 0: U(0); 0 < k < L: U(k) U(k-1); k = L: U(L-1)), phase
+    // gamma_k = tau B(s_{k-1}) on the J-only energy before mixer k (gamma_0 = 0)
+    const int p = L + 1;
+    std::vector<double2> G((size_t)p * n * 4);
+    std::vector<double> gam(p, 0.0), bet(p, 0.0);
+    for (int k = 0; k < p; ++k) {
+        if (k > 0) gam[k] = tau * pwl(s, B, n_knots, (double)(k - 1) / (double)L);
+        for (int a = 0; a < n; ++a) {
+            std::complex<double> M[4];
+            if (k == 0 || k == L) {
+                half(k == 0 ? 0 : L - 1, a, M);
+            } else {
+                std::complex<double> Ua[4], Ub[4];
+                half(k - 1, a, Ua);
+                half(k, a, Ub);
+                M[0] = Ub[0] * Ua[0] + Ub[1] * Ua[2];
+                M[1] = Ub[0] * Ua[1] + Ub[1] * Ua[3];
+                M[2] = Ub[2] * Ua[0] + Ub[3] * Ua[2];
+                M[3] = Ub[2] * Ua[1] + Ub[3] * Ua[3];
+            }
+            for (int e = 0; e < 4; ++e) G[((size_t)k * n + a) * 4 + e] = make_double2(M[e].real(), M[e].imag());
+        }
+    }
+    q->gmats = &G;
+    q->frame_noh = true;
+    q->res_valid = false;
+    int rc = apply_layers(q, gam.data(), bet.data(), p);
+    if (rc == QSIM_OK) rc = qsim_sync(q) == QSIM_OK ? QSIM_OK : QSIM_ECUDA;  // G must outlive the launches
+    q->gmats = nullptr;
+    q->frame_noh = false;
+    q->res_valid = false;
+    return rc;
 }
 
 int qsim_expect_hc(qsim_t *q, double *out) {

@@ -143,6 +143,40 @@ __device__ __forceinline__ void mix_frame(double2 (&v)[NR], unsigned mask, doubl
     if (m5 & 16) bfly<4>(v, t);
 }
 
+// general 2x2 butterfly: (a, b) <- (m00 a + m01 b, m10 a + m11 b)
+__device__ __forceinline__ double2 cmac(double2 m, double2 x, double2 acc) {
+    return make_double2(fma(m.x, x.x, fma(-m.y, x.y, acc.x)), fma(m.x, x.y, fma(m.y, x.x, acc.y)));
+}
+template <int RBIT>
+__device__ __forceinline__ void gbfly(double2 (&v)[NR], const double2 (&M)[4]) {
+    const double2 m00 = M[0], m01 = M[1], m10 = M[2], m11 = M[3];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+        if (j & (1 << RBIT)) continue;
+        const double2 a = v[j], b = v[j | (1 << RBIT)];
+        v[j] = cmac(m00, a, cmac(m01, b, make_double2(0.0, 0.0)));
+        v[j | (1 << RBIT)] = cmac(m10, a, cmac(m11, b, make_double2(0.0, 0.0)));
+    }
+}
+// `skew`: register bits whose tile bit is inverted in this lane (the lane-skewed frame Y of the
+// TMA kernel); there register slot 0 holds the |1> amplitude, so the lane applies X M X
+template <int RBIT>
+__device__ __forceinline__ void gbfly_sk(double2 (&v)[NR], const double2 (&M)[4], int skew) {
+    const bool sw = (skew >> RBIT) & 1;
+    const double2 G[4] = {sw ? M[3] : M[0], sw ? M[2] : M[1], sw ? M[1] : M[2], sw ? M[0] : M[3]};
+    gbfly<RBIT>(v, G);
+}
+template <int F>
+__device__ __forceinline__ void gmix_frame(double2 (&v)[NR], unsigned mask, const double2 (&G)[KT][4],
+                                           int skew = 0) {
+    const unsigned m5 = (mask >> Frame<F>::RB) & 0x1Fu;
+    if (m5 & 1) gbfly_sk<0>(v, G[Frame<F>::RB + 0], skew);
+    if (m5 & 2) gbfly_sk<1>(v, G[Frame<F>::RB + 1], skew);
+    if (m5 & 4) gbfly_sk<2>(v, G[Frame<F>::RB + 2], skew);
+    if (m5 & 8) gbfly<3>(v, G[Frame<F>::RB + 3]);
+    if (m5 & 16) gbfly<4>(v, G[Frame<F>::RB + 4]);
+}
+
 // frame change through shared memory (one barrier); every thread writes back exactly
 // the elements it read in the previous exchange, so one barrier per exchange suffices.
 template <int F1, int F2>

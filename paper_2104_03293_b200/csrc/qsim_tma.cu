@@ -203,7 +203,14 @@ __device__ __forceinline__ void store_tile_swapped(const double2 (&v)[NR], const
     }
 }
 
-template <int KIND>
+// the mixer of a frame: scaled R_x butterflies, or the general per-bit 2x2 (GMIX)
+#define MIXF(FR, MASK, WHICH)                                                             \
+    do {                                                                                  \
+        if (GMIX) gmix_frame<FR>(v, (MASK), (WHICH) == 1 ? P.gm1 : P.gm2, FR == FY ? (lane & 7) : 0); \
+        else mix_frame<FR>(v, (MASK), (WHICH) == 1 ? P.c1.t : P.c2.t);                     \
+    } while (0)
+
+template <int KIND, bool GMIX>
 __global__ void __launch_bounds__(TMA_NG * 128, 1)
     tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -280,19 +287,19 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         // ------------------------------------------------ rounds up to the last smem read
         if (load_state) {
             lds_frame<FX>(v, sm, lane, warp);
-            mix_frame<FX>(v, P.mix1 & TMX, P.c1.t);
+            MIXF(FX, P.mix1 & TMX, 1);
             sts_frame<FX>(v, sm, lane, warp);
             group_bar(g);
             if (RUN) {
                 lds_frame<FW>(v, sm, lane, warp);
-                if (TURN) mix_frame<FW>(v, P.mix1 & TMW, P.c1.t);
+                if (TURN) MIXF(FW, P.mix1 & TMW, 1);
             } else {
                 lds_frame<FY>(v, sm, lane, warp);
-                mix_frame<FY>(v, P.mix1 & TMY, P.c1.t);
+                MIXF(FY, P.mix1 & TMY, 1);
                 sts_frame<FY>(v, sm, lane, warp);
                 group_bar(g);
                 lds_frame<FZ>(v, sm, lane, warp);
-                if (TURN) mix_frame<FZ>(v, P.mix1 & TMZ, P.c1.t);
+                if (TURN) MIXF(FZ, P.mix1 & TMZ, 1);
             }
         } else {
 #pragma unroll
@@ -301,15 +308,15 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         if (TURN) {
             apply_phase<FE>(v, R, tE, fr, pconst, u, cs.PRR);
             if (RUN) {
-                mix_frame<FW>(v, P.mix2 & TMW, P.c2.t);
+                MIXF(FW, P.mix2 & TMW, 2);
                 sts_frame<FW>(v, sm, lane, warp);
                 group_bar(g);
             } else {
-                mix_frame<FZ>(v, P.mix2 & TMZ, P.c2.t);
+                MIXF(FZ, P.mix2 & TMZ, 2);
                 sts_frame<FZ>(v, sm, lane, warp);
                 group_bar(g);
                 lds_frame<FY>(v, sm, lane, warp);
-                mix_frame<FY>(v, P.mix2 & TMY, P.c2.t);
+                MIXF(FY, P.mix2 & TMY, 2);
                 sts_frame<FY>(v, sm, lane, warp);
                 group_bar(g);
             }
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         }
         // ------------------------------------------------ finish in registers, store
         if (TURN) {
-            mix_frame<FX>(v, P.mix2 & TMX, P.c2.t);
+            MIXF(FX, P.mix2 & TMX, 2);
             if (P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
             else if (P.tmo) store_tile_major<FX>(v, P, ut, lane, warp);
             else if (tstore) {
@@ -345,8 +352,8 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             } else
                 store_tile<FX>(v, P.psi + tb + offX, P.L);
         } else {
-            if (RUN) mix_frame<FW>(v, P.mix1 & TMW, P.c1.t);
-            else mix_frame<FZ>(v, P.mix1 & TMZ, P.c1.t);
+            if (RUN) MIXF(FW, P.mix1 & TMW, 1);
+            else MIXF(FZ, P.mix1 & TMZ, 1);
             if (P.dbg & 1) {  // diagnostics: read-only pass (keep the values alive)
                 double s = 0.0;
 #pragma unroll
@@ -409,27 +416,39 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
 
 size_t tma_smem_bytes() { return TmaSmem::total; }
 
-cudaError_t setup_tma_kernels() {
+template <bool GMIX>
+cudaError_t setup_tma_kernels_g() {
     cudaError_t e;
-    e = cudaFuncSetAttribute(tma_pass_kernel<K_PLAIN12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
+    e = cudaFuncSetAttribute(tma_pass_kernel<K_PLAIN12, GMIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(tma_pass_kernel<K_PLAIN_RUN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
+    e = cudaFuncSetAttribute(tma_pass_kernel<K_PLAIN_RUN, GMIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(tma_pass_kernel<K_TURN12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
+    e = cudaFuncSetAttribute(tma_pass_kernel<K_TURN12, GMIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(tma_pass_kernel<K_TURN_RUN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
+    return cudaFuncSetAttribute(tma_pass_kernel<K_TURN_RUN, GMIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
 }
 
-cudaError_t launch_tma_pass(const CUtensorMap &tm, const PassParams &P, int grid, cudaStream_t s) {
+cudaError_t setup_tma_kernels() {
+    cudaError_t e = setup_tma_kernels_g<false>();
+    if (e != cudaSuccess) return e;
+    return setup_tma_kernels_g<true>();
+}
+
+template <bool GMIX>
+cudaError_t launch_tma_pass_g(const CUtensorMap &tm, const PassParams &P, int grid, cudaStream_t s) {
     const size_t sh = TmaSmem::total;
     switch (P.kind) {
-        case K_PLAIN12: tma_pass_kernel<K_PLAIN12><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
-        case K_PLAIN_RUN: tma_pass_kernel<K_PLAIN_RUN><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
-        case K_TURN12: tma_pass_kernel<K_TURN12><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
-        case K_TURN_RUN: tma_pass_kernel<K_TURN_RUN><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
+        case K_PLAIN12: tma_pass_kernel<K_PLAIN12, GMIX><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
+        case K_PLAIN_RUN: tma_pass_kernel<K_PLAIN_RUN, GMIX><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
+        case K_TURN12: tma_pass_kernel<K_TURN12, GMIX><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
+        case K_TURN_RUN: tma_pass_kernel<K_TURN_RUN, GMIX><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
+}
+
+cudaError_t launch_tma_pass(const CUtensorMap &tm, const PassParams &P, int grid, cudaStream_t s) {
+    return P.gmix ? launch_tma_pass_g<true>(tm, P, grid, s) : launch_tma_pass_g<false>(tm, P, grid, s);
 }
 
 }  // namespace qk

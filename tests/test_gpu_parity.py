@@ -367,3 +367,45 @@ def test_ground_states_full_size_exact_cover(Q, big30):
     z_star = int(sum(int(x_star[i]) << i for i in range(n)))
     assert emin + C == 0.0 and z_star in gs and cnt >= 1
     assert o.energy(h, J, gs[0]) == emin
+
+
+# ------------------------------------------------------------------ NEXT-1: QSDS combined step
+@pytest.mark.parametrize("n,steps", [(6, 4), (12, 3), (15, 5), (22, 3)])
+def test_qsds_parity(Q, n, steps):
+    h, J = inst.random_ising(n, 700 + n)
+    s_, A, B = inst.dw_like_schedule()
+    A, B = 2 * np.pi * A / 10, 2 * np.pi * B / 10
+    tau = 0.4
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        s.init_plus()
+        s.apply_qsds(tau, steps, s_, A, B)
+        psi = s.amplitudes()
+        e = s.expect_hc()
+    ref = o.qsds_state(h, J, tau, steps, s_, A, B)
+    assert_state_close(psi, ref)
+    assert_expect_close(e, h, J, ref)
+
+
+def test_qsds_after_flipped_qaoa(Q):
+    """QSDS continuing a state whose qubits carry X-gate flips (|tan beta| > 1 mixers)."""
+    n = 16
+    h, J = inst.random_ising(n, 55)
+    s_, A, B = inst.toy_schedule()
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        s.init_plus()
+        s.apply_qaoa([0.7, -0.4], [1.3, 2.2])
+        s.apply_qsds(0.3, 3, s_, A, B)
+        psi = s.amplitudes()
+    ref = o.qaoa_state(h, J, [0.7, -0.4], [1.3, 2.2])
+    # continue the oracle state with the QSDS steps: compose via a fresh oracle run on |ref>
+    import oracle.oracle as oo
+    tau, steps = 0.3, 3
+    cur = ref.copy()
+    L = oo.lib()
+    import ctypes
+    L.oracle_apply_qsds(n, oo._dp(np.ascontiguousarray(h)), oo._dp(np.ascontiguousarray(J)), tau, steps,
+                        oo._dp(np.ascontiguousarray(s_, dtype=float)), oo._dp(np.ascontiguousarray(A, dtype=float)),
+                        oo._dp(np.ascontiguousarray(B, dtype=float)), len(s_), oo._dp(cur.view(np.float64)))
+    assert_state_close(psi, cur)

@@ -94,6 +94,17 @@ for n in a.qubits:
         report(f"n={n} spins", np.max(np.abs(sz - o.spin_expectations(ref))) <= 1e-11)
         rgs, remin, rcnt = o.ground_states(h, J, max_out=8)
         report(f"n={n} ground states", emin == remin and cnt == rcnt and gs == rgs[: len(gs)])
+    # 1c) QSDS combined stepping (NEXT-1) on the sharded handle
+    s_, A, B = inst.toy_schedule()
+    sim = Q.QSim(n, rank=rank, world=world, nccl_unique_id=new_uid())
+    sim.set_ising(h, J)
+    sim.init_plus()
+    sim.apply_qsds(0.35, 3, s_, A, B)
+    psi_q = sim.amplitudes() if n <= 24 else None
+    sim.close()
+    if rank == 0 and n <= 24:
+        ref = o.qsds_state(h, J, 0.35, 3, s_, A, B)
+        report(f"n={n} QSDS amplitudes", np.max(np.abs(psi_q - ref)) <= 1e-10)
     # 1b) p = 1 closed-form <H_C> (pin P4), any n
     sim = Q.QSim(n, rank=rank, world=world, nccl_unique_id=new_uid())
     sim.set_ising(h, J)
