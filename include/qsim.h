@@ -118,6 +118,11 @@ int qsim_apply_aqa(qsim_t *q, double T, int p, const double *s, const double *A,
 int qsim_apply_qsds(qsim_t *q, double tau, int n_steps, const double *s, const double *A, const double *B,
                     int n_knots);
 
+/* apply `reps` layers of H on every qubit, (H^{otimes n})^reps -- the paper's
+ * Hadamard benchmark circuit (H^N)^11 (Table I) -- with the general-mixer tile passes
+ * (12 gates per HBM sweep); no phase. */
+int qsim_apply_hadamard(qsim_t *q, int reps);
+
 /* Host-only helper (no device work): the angles qsim_apply_aqa uses. */
 int qsim_aqa_angles(double T, int p, const double *s, const double *A, const double *B,
                     int n_knots, double *gamma_out, double *beta_out);

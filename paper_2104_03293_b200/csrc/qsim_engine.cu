@@ -1233,6 +1233,32 @@ int qsim_apply_qsds(qsim_t *q, double tau, int n_steps, const double *s, const d
     return rc;
 }
 
+int qsim_apply_hadamard(qsim_t *q, int reps) {
+    if (!q) return QSIM_EINVAL;
+    if (reps < 1) return fail(q, QSIM_EINVAL, "reps >= 1");
+    if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
+    if (!q->use_tma && q->m > qk::KT) return fail(q, QSIM_EUNSUPPORTED, "needs the TMA pass kernel");
+    const int n = q->n;
+    const double r = std::sqrt(0.5);
+    std::vector<double2> G((size_t)reps * n * 4);
+    for (size_t i = 0; i < (size_t)reps * n; ++i) {
+        G[4 * i + 0] = make_double2(r, 0.0);
+        G[4 * i + 1] = make_double2(r, 0.0);
+        G[4 * i + 2] = make_double2(r, 0.0);
+        G[4 * i + 3] = make_double2(-r, 0.0);
+    }
+    std::vector<double> zero(reps, 0.0);
+    q->gmats = &G;
+    q->frame_noh = true;
+    q->res_valid = false;
+    int rc = apply_layers(q, zero.data(), zero.data(), reps);
+    if (rc == QSIM_OK) rc = qsim_sync(q) == QSIM_OK ? QSIM_OK : QSIM_ECUDA;
+    q->gmats = nullptr;
+    q->frame_noh = false;
+    q->res_valid = false;
+    return rc;
+}
+
 int qsim_expect_hc(qsim_t *q, double *out) {
     if (!q) return QSIM_EINVAL;
     if (!out) return fail(q, QSIM_EINVAL, "out is NULL");

@@ -306,7 +306,8 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             for (int j = 0; j < NR; ++j) v[j] = make_double2(P.a0, 0.0);
         }
         if (TURN) {
-            apply_phase<FE>(v, R, tE, fr, pconst, u, cs.PRR);
+            if (!(GMIX && P.gamma == 0.0 && P.scale.x == 1.0 && P.scale.y == 0.0))  // identity phase
+                apply_phase<FE>(v, R, tE, fr, pconst, u, cs.PRR);
             if (RUN) {
                 MIXF(FW, P.mix2 & TMW, 2);
                 sts_frame<FW>(v, sm, lane, warp);

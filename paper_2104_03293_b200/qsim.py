@@ -34,7 +34,7 @@ _ERRNAMES = {QSIM_EINVAL: "EINVAL", QSIM_ENOMEM: "ENOMEM", QSIM_ERANGE: "ERANGE"
 
 # every symbol include/qsim.h declares (tests check the library exports all of them)
 EXPORTS = ["qsim_create", "qsim_create_ex", "qsim_destroy", "qsim_set_ising", "qsim_init_plus",
-           "qsim_apply_qaoa", "qsim_apply_aqa", "qsim_apply_qsds", "qsim_aqa_angles", "qsim_expect_hc", "qsim_norm2",
+           "qsim_apply_qaoa", "qsim_apply_aqa", "qsim_apply_qsds", "qsim_apply_hadamard", "qsim_aqa_angles", "qsim_expect_hc", "qsim_norm2",
            "qsim_success_prob", "qsim_get_amplitudes", "qsim_energies", "qsim_spin_expectations",
            "qsim_apply_aqa_traced", "qsim_ground_states", "qsim_enumerate", "qsim_sync",
            "qsim_plan_counts", "qsim_plan_positions", "qsim_nccl_unique_id",
@@ -66,6 +66,7 @@ lib.qsim_init_plus.argtypes = [_H]
 lib.qsim_apply_qaoa.argtypes = [_H, _D, _D, ctypes.c_int]
 lib.qsim_apply_aqa.argtypes = [_H, ctypes.c_double, ctypes.c_int, _D, _D, _D, ctypes.c_int]
 lib.qsim_apply_qsds.argtypes = [_H, ctypes.c_double, ctypes.c_int, _D, _D, _D, ctypes.c_int]
+lib.qsim_apply_hadamard.argtypes = [_H, ctypes.c_int]
 lib.qsim_aqa_angles.argtypes = [ctypes.c_double, ctypes.c_int, _D, _D, _D, ctypes.c_int, _D, _D]
 lib.qsim_expect_hc.argtypes = [_H, _D]
 lib.qsim_norm2.argtypes = [_H, _D]
@@ -153,6 +154,10 @@ def qsim_apply_aqa(h, T: float, p: int, s, A, B) -> None:
 def qsim_apply_qsds(h, tau: float, n_steps: int, s, A, B) -> None:
     s, A, B = _f64(s), _f64(A), _f64(B)
     _check(lib.qsim_apply_qsds(h, float(tau), int(n_steps), _dp(s), _dp(A), _dp(B), int(s.shape[0])), h)
+
+
+def qsim_apply_hadamard(h, reps: int) -> None:
+    _check(lib.qsim_apply_hadamard(h, int(reps)), h)
 
 
 def qsim_aqa_angles(T: float, p: int, s, A, B):
@@ -331,6 +336,9 @@ class QSim:
 
     def apply_qsds(self, tau, n_steps, s, A, B):
         qsim_apply_qsds(self.h, tau, n_steps, s, A, B)
+
+    def apply_hadamard(self, reps):
+        qsim_apply_hadamard(self.h, reps)
 
     def expect_hc(self):
         return qsim_expect_hc(self.h)

@@ -409,3 +409,30 @@ def test_qsds_after_flipped_qaoa(Q):
                         oo._dp(np.ascontiguousarray(s_, dtype=float)), oo._dp(np.ascontiguousarray(A, dtype=float)),
                         oo._dp(np.ascontiguousarray(B, dtype=float)), len(s_), oo._dp(cur.view(np.float64)))
     assert_state_close(psi, cur)
+
+
+# ------------------------------------------------------------------ NEXT-4: Hadamard circuits
+@pytest.mark.parametrize("n", [8, 14, 21])
+def test_hadamard_layers(Q, n):
+    """(H^n)^11 |+> = |0>; (H^n)^2 = identity; a random state after 3 layers vs dense."""
+    h, J = inst.random_ising(n, 3)
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        s.init_plus()
+        s.apply_hadamard(11)
+        psi = s.amplitudes()
+        ref = np.zeros(1 << n, dtype=complex)
+        ref[0] = 1.0
+        assert np.max(np.abs(psi - ref)) <= 1e-12
+        g, b = rand_angles(2, n)
+        s.init_plus()
+        s.apply_qaoa(g, b)
+        s.apply_hadamard(3)
+        psi3 = s.amplitudes()
+    st = o.qaoa_state(h, J, g, b)
+    # H^{otimes n} = normalised Walsh-Hadamard transform (qubit j <-> bit j)
+    wht = st.copy()
+    for q in range(n):
+        wht = wht.reshape(-1, 2, 1 << q)
+        wht = np.stack([wht[:, 0] + wht[:, 1], wht[:, 0] - wht[:, 1]], axis=1).reshape(-1) / np.sqrt(2)
+    assert np.max(np.abs(psi3 - wht)) <= 1e-12

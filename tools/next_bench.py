@@ -62,9 +62,25 @@ ps_q = sim.success_prob([z_star])
 ms_a = timed(aqa)
 ps_a = sim.success_prob([z_star])
 ms_s = timed(lambda: sim.spins(), reps=3)
+
+
+def hadamard():
+    sim.init_plus()
+    sim.apply_hadamard(11)
+
+
+ms_h = timed(hadamard, reps=2)
+amp0 = sim.amplitudes(0, 1)[0]
 print(json.dumps({"row": "NEXT-1 QSDS combined step", "n": n, "step_operators": a.steps,
                   "ms_total": ms_q, "ms_per_step": ms_q / a.steps, "p_success": ps_q,
                   "split_form_ms_per_layer": ms_a / a.steps, "split_form_p_success": ps_a}))
 print(json.dumps({"row": "NEXT-2 <sigma^z_i> sweep", "n": n, "ms": ms_s,
                   "GB_per_s": 16 * 2.0 ** n / (ms_s / 1e3) / 1e9}))
+gates = 11 * n
+print(json.dumps({"row": "NEXT-4 Hadamard (H^N)^11 (P:177)", "n": n, "ms": ms_h, "gates": gates,
+                  "gate_amplitude_updates_per_s": gates * 2.0 ** n / (ms_h / 1e3),
+                  "normalized_time_s_to_32_gates": 352.0 / gates * ms_h / 1e3,
+                  "amp0_of_final_state": [amp0.real, amp0.imag],
+                  "paper_context": "JUQCS-G A100 compute-only ~5.5e10 gate-amplitude updates/s per GPU "
+                                   "(derived from P:197, P:177; precision not stated, likely FP32)"}))
 sim.close()
