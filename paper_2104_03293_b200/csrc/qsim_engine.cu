@@ -268,6 +268,7 @@ struct qsim {
     // general-mixer mode (QSDS combined step): per layer, per logical qubit a 2x2 matrix; the
     // phase uses the J-only frame (frame_noh)
     const std::vector<double2> *gmats = nullptr;  // [layer][qubit][4]
+    bool hmode = false;        // Hadamard layers (gmats holds H): dedicated butterfly
     bool frame_noh = false;
     bool fr_noh_built = false;
     bool tilemajor = false;    // single GPU: out-of-place relabelling schedule (second buffer)
@@ -545,6 +546,13 @@ int prof_events(qsim *q, cudaEvent_t *a, cudaEvent_t *b) {
 void set_gmix(const qsim *q, qk::PassParams &P, const int *L, const PassOp &op) {
     if (!q->gmats) return;
     const std::vector<double2> &G = *q->gmats;
+    if (q->hmode) {  // (a + b, a - b) butterflies, 2^{-|mixed|/2} once per pass; flips commute
+        P.gmix = 2;
+        P.c1.form = P.c2.form = 0;
+        const int nm = __builtin_popcount(P.mix1) + __builtin_popcount(P.mix2);
+        P.scale = make_double2(std::pow(0.5, 0.5 * nm), 0.0);
+        return;
+    }
     P.gmix = 1;
     P.c1.form = P.c2.form = 0;
     P.c1.t = P.c2.t = 0.0;
@@ -1249,11 +1257,13 @@ int qsim_apply_hadamard(qsim_t *q, int reps) {
     }
     std::vector<double> zero(reps, 0.0);
     q->gmats = &G;
+    q->hmode = q->m > qk::KT;  // the tile kernels have a dedicated Hadamard butterfly
     q->frame_noh = true;
     q->res_valid = false;
     int rc = apply_layers(q, zero.data(), zero.data(), reps);
     if (rc == QSIM_OK) rc = qsim_sync(q) == QSIM_OK ? QSIM_OK : QSIM_ECUDA;
     q->gmats = nullptr;
+    q->hmode = false;
     q->frame_noh = false;
     q->res_valid = false;
     return rc;

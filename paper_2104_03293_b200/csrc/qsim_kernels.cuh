@@ -158,6 +158,43 @@ __device__ __forceinline__ void gbfly(double2 (&v)[NR], const double2 (&M)[4]) {
         v[j | (1 << RBIT)] = cmac(m10, a, cmac(m11, b, make_double2(0.0, 0.0)));
     }
 }
+// Hadamard butterfly without its 1/sqrt2 (applied once per pass): (a, b) <- (a + b, a - b)
+template <int RBIT>
+__device__ __forceinline__ void hbfly(double2 (&v)[NR]) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+        if (j & (1 << RBIT)) continue;
+        const double2 a = v[j], b = v[j | (1 << RBIT)];
+        v[j] = make_double2(a.x + b.x, a.y + b.y);
+        v[j | (1 << RBIT)] = make_double2(a.x - b.x, a.y - b.y);
+    }
+}
+// In a lane-skewed or flipped slot (register slot 0 holds the |1> amplitude) the lane applies
+// X H X: (slot0, slot1) <- (slot1 - slot0, slot1 + slot0)
+template <int RBIT>
+__device__ __forceinline__ void hbfly_sk(double2 (&v)[NR], int skew) {
+    if ((skew >> RBIT) & 1) {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+            if (j & (1 << RBIT)) continue;
+            const double2 a = v[j], b = v[j | (1 << RBIT)];  // a holds |1>, b holds |0>
+            v[j] = make_double2(b.x - a.x, b.y - a.y);         // new |1> = (|0> - |1>)
+            v[j | (1 << RBIT)] = make_double2(b.x + a.x, b.y + a.y);
+        }
+    } else {
+        hbfly<RBIT>(v);
+    }
+}
+template <int F>
+__device__ __forceinline__ void hmix_frame(double2 (&v)[NR], unsigned mask, int skew = 0) {
+    const unsigned m5 = (mask >> Frame<F>::RB) & 0x1Fu;
+    if (m5 & 1) hbfly_sk<0>(v, skew);
+    if (m5 & 2) hbfly_sk<1>(v, skew);
+    if (m5 & 4) hbfly_sk<2>(v, skew);
+    if (m5 & 8) hbfly_sk<3>(v, skew);
+    if (m5 & 16) hbfly_sk<4>(v, skew);
+}
+
 // `skew`: register bits whose tile bit is inverted in this lane (the lane-skewed frame Y of the
 // TMA kernel); there register slot 0 holds the |1> amplitude, so the lane applies X M X
 template <int RBIT>

@@ -204,13 +204,15 @@ __device__ __forceinline__ void store_tile_swapped(const double2 (&v)[NR], const
 }
 
 // the mixer of a frame: scaled R_x butterflies, or the general per-bit 2x2 (GMIX)
+// mixer modes: GMIX 0 = scaled R_x, 1 = general per-bit 2x2, 2 = Hadamard
 #define MIXF(FR, MASK, WHICH)                                                             \
     do {                                                                                  \
-        if (GMIX) gmix_frame<FR>(v, (MASK), (WHICH) == 1 ? P.gm1 : P.gm2, FR == FY ? (lane & 7) : 0); \
+        if (GMIX == 1) gmix_frame<FR>(v, (MASK), (WHICH) == 1 ? P.gm1 : P.gm2, FR == FY ? (lane & 7) : 0); \
+        else if (GMIX == 2) hmix_frame<FR>(v, (MASK), (FR == FY ? (lane & 7) : 0) ^ ((ft >> Frame<FR>::RB) & 31)); \
         else mix_frame<FR>(v, (MASK), (WHICH) == 1 ? P.c1.t : P.c2.t);                     \
     } while (0)
 
-template <int KIND, bool GMIX>
+template <int KIND, int GMIX>
 __global__ void __launch_bounds__(TMA_NG * 128, 1)
     tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -306,7 +308,10 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             for (int j = 0; j < NR; ++j) v[j] = make_double2(P.a0, 0.0);
         }
         if (TURN) {
-            if (!(GMIX && P.gamma == 0.0 && P.scale.x == 1.0 && P.scale.y == 0.0))  // identity phase
+            if (GMIX == 2) {  // no phase; the pass-wide 2^{-m/2} of the Hadamards
+#pragma unroll
+                for (int j = 0; j < NR; ++j) v[j] = make_double2(v[j].x * P.scale.x, v[j].y * P.scale.x);
+            } else if (!(GMIX == 1 && P.gamma == 0.0 && P.scale.x == 1.0 && P.scale.y == 0.0))  // identity phase
                 apply_phase<FE>(v, R, tE, fr, pconst, u, cs.PRR);
             if (RUN) {
                 MIXF(FW, P.mix2 & TMW, 2);
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
 
 size_t tma_smem_bytes() { return TmaSmem::total; }
 
-template <bool GMIX>
+template <int GMIX>
 cudaError_t setup_tma_kernels_g() {
     cudaError_t e;
     e = cudaFuncSetAttribute(tma_pass_kernel<K_PLAIN12, GMIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
@@ -430,12 +435,14 @@ cudaError_t setup_tma_kernels_g() {
 }
 
 cudaError_t setup_tma_kernels() {
-    cudaError_t e = setup_tma_kernels_g<false>();
+    cudaError_t e = setup_tma_kernels_g<0>();
     if (e != cudaSuccess) return e;
-    return setup_tma_kernels_g<true>();
+    e = setup_tma_kernels_g<1>();
+    if (e != cudaSuccess) return e;
+    return setup_tma_kernels_g<2>();
 }
 
-template <bool GMIX>
+template <int GMIX>
 cudaError_t launch_tma_pass_g(const CUtensorMap &tm, const PassParams &P, int grid, cudaStream_t s) {
     const size_t sh = TmaSmem::total;
     switch (P.kind) {
@@ -449,7 +456,12 @@ cudaError_t launch_tma_pass_g(const CUtensorMap &tm, const PassParams &P, int gr
 }
 
 cudaError_t launch_tma_pass(const CUtensorMap &tm, const PassParams &P, int grid, cudaStream_t s) {
-    return P.gmix ? launch_tma_pass_g<true>(tm, P, grid, s) : launch_tma_pass_g<false>(tm, P, grid, s);
+    switch (P.gmix) {
+        case 0: return launch_tma_pass_g<0>(tm, P, grid, s);
+        case 1: return launch_tma_pass_g<1>(tm, P, grid, s);
+        case 2: return launch_tma_pass_g<2>(tm, P, grid, s);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace qk

@@ -436,3 +436,21 @@ def test_hadamard_layers(Q, n):
         wht = wht.reshape(-1, 2, 1 << q)
         wht = np.stack([wht[:, 0] + wht[:, 1], wht[:, 0] - wht[:, 1]], axis=1).reshape(-1) / np.sqrt(2)
     assert np.max(np.abs(psi3 - wht)) <= 1e-12
+
+
+def test_hadamard_after_flipped_qaoa(Q):
+    """Hadamard layers on a state whose qubits carry X-gate flips (|tan beta| > 1 mixers)."""
+    n = 17
+    h, J = inst.random_ising(n, 4)
+    g, b = [0.5, -0.9], [1.2, 2.4]
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        s.init_plus()
+        s.apply_qaoa(g, b)
+        s.apply_hadamard(1)
+        psi = s.amplitudes()
+    wht = o.qaoa_state(h, J, g, b)
+    for q in range(n):
+        wht = wht.reshape(-1, 2, 1 << q)
+        wht = np.stack([wht[:, 0] + wht[:, 1], wht[:, 0] - wht[:, 1]], axis=1).reshape(-1) / np.sqrt(2)
+    assert np.max(np.abs(psi - wht)) <= 1e-12
