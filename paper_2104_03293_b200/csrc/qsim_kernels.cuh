@@ -214,6 +214,23 @@ __device__ __forceinline__ void gmix_frame(double2 (&v)[NR], unsigned mask, cons
     if (m5 & 16) gbfly<4>(v, G[Frame<F>::RB + 4]);
 }
 
+// runtime-frame variants (one copy of code for every frame): element t = tthr | ((j ^ sk) << rb)
+__device__ __forceinline__ void mix5(double2 (&v)[NR], unsigned m5, double t) {
+    if (m5 & 1) bfly<0>(v, t);
+    if (m5 & 2) bfly<1>(v, t);
+    if (m5 & 4) bfly<2>(v, t);
+    if (m5 & 8) bfly<3>(v, t);
+    if (m5 & 16) bfly<4>(v, t);
+}
+__device__ __forceinline__ void lds_rt(double2 (&v)[NR], const double2 *sm, int tthr, int rb) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) v[j] = sm[tthr | (j << rb)];
+}
+__device__ __forceinline__ void sts_rt(const double2 (&v)[NR], double2 *sm, int tthr, int rb) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) sm[tthr | (j << rb)] = v[j];
+}
+
 // frame change through shared memory (one barrier); every thread writes back exactly
 // the elements it read in the previous exchange, so one barrier per exchange suffices.
 template <int F1, int F2>

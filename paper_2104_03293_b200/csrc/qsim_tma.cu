@@ -286,6 +286,60 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         double2 *sm = stages + (size_t)s * TILE;
         const TileRec *R = srec + s;
         if (load_state || need_e) wait_tile(I, i);
+        // ------------------------------------------------ compact turning-run body
+        // (instruction-cache footprint: one copy of the butterflies, the smem sweeps and the
+        // phase, driven by four mix steps X(mix1) W(mix1) [phase] W(mix2) X(mix2))
+        if constexpr (KIND == K_TURN_RUN && GMIX == 0) {
+            const int tXt = Frame<FX>::tthr(lane, warp), tWt = Frame<FW>::tthr(lane, warp);
+            const unsigned mx1 = (P.mix1 & TMX) >> 7, mw1 = (P.mix1 & TMW) >> 3;
+            const unsigned mw2 = (P.mix2 & TMW) >> 3, mx2 = (P.mix2 & TMX) >> 7;
+            if (!load_state) {
+#pragma unroll
+                for (int j = 0; j < NR; ++j) v[j] = make_double2(P.a0, 0.0);
+            }
+            int prev = -1;  // frame of the registers: 0 = X, 1 = W
+#pragma unroll 1
+            for (int stp = load_state ? 0 : 2; stp < 4; ++stp) {
+                const int fr_now = (stp == 1 || stp == 2) ? 1 : 0;
+                if (load_state && fr_now != prev) {
+                    if (prev >= 0) {
+                        sts_rt(v, sm, prev ? tWt : tXt, prev ? Frame<FW>::RB : Frame<FX>::RB);
+                        group_bar(g);
+                    }
+                    lds_rt(v, sm, fr_now ? tWt : tXt, fr_now ? Frame<FW>::RB : Frame<FX>::RB);
+                } else if (!load_state && stp == 3) {
+                    sts_rt(v, sm, tWt, Frame<FW>::RB);
+                    group_bar(g);
+                    lds_rt(v, sm, tXt, Frame<FX>::RB);
+                }
+                prev = fr_now;
+                if (stp == 2) apply_phase<FW>(v, R, tE, fr, pconst, u, cs.PRR);
+                if (stp == 3) {  // last smem read done: release the stage unless TMA-storing
+                    if (!(P.tma_store && !P.swap_store && !P.tmo)) {
+                        fence_async_smem();
+                        group_bar(g);
+                        if (gt == 0 && i + NSTAGE < ntl)
+                            issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                    }
+                }
+                mix5(v, stp == 0 ? mx1 : stp == 1 ? mw1 : stp == 2 ? mw2 : mx2, stp < 2 ? P.c1.t : P.c2.t);
+            }
+            if (P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
+            else if (P.tmo) store_tile_major<FX>(v, P, ut, lane, warp);
+            else if (P.tma_store) {
+                sts_rt(v, sm, tXt, Frame<FX>::RB);
+                fence_async_smem();
+                group_bar(g);
+                if (gt == 0) {
+                    int c[5];
+                    tile_coords(P, ut, c);
+                    tma_store_5d(I.tm, c, sm, (P.l2hint >> 2) & 3);
+                    bulk_wait_read0();
+                    if (i + NSTAGE < ntl) issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                }
+            } else
+                store_tile<FX>(v, P.psi + tb + offX, P.L);
+        } else {
         // ------------------------------------------------ rounds up to the last smem read
         if (load_state) {
             lds_frame<FX>(v, sm, lane, warp);
@@ -394,6 +448,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             if (P.tmo) store_tile_major<RUN ? FW : FZ>(v, P, ut, lane, warp);
             else store_tile<RUN ? FW : FZ>(v, P.psi + tb + offS, P.L);
         }
+        }  // generic body
     }
     if (P.swap_store) __threadfence_system();  // NVLink stores visible before the pass completes
     if (P.reduce) {
