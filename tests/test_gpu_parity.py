@@ -454,3 +454,70 @@ def test_hadamard_after_flipped_qaoa(Q):
         wht = wht.reshape(-1, 2, 1 << q)
         wht = np.stack([wht[:, 0] + wht[:, 1], wht[:, 0] - wht[:, 1]], axis=1).reshape(-1) / np.sqrt(2)
     assert np.max(np.abs(psi - wht)) <= 1e-12
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("n", [13, 15, 17, 19, 21])
+def test_all_set_layouts_p1_p2(Q, n):
+    """Every tile-set count (runs of 1..9 bits), p = 1 (no turning pass) and p = 2."""
+    h, J = inst.random_ising(n, 1000 + n)
+    for p in (1, 2):
+        g, b = rand_angles(p, 1100 + n + p)
+        psi, e, nrm, _ = run_gpu(Q, h, J, g, b)
+        ref = o.qaoa_state(h, J, g, b)
+        assert_state_close(psi, ref)
+        assert_expect_close(e, h, J, ref)
+
+
+def test_aqa_minimum_p(Q):
+    n = 14
+    h, J = inst.random_ising(n, 8)
+    s_, A, B = inst.toy_schedule()
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        s.init_plus()
+        s.apply_aqa(1.0, 2, s_, A, B)
+        psi = s.amplitudes()
+    assert_state_close(psi, o.aqa_state(h, J, 1.0, 2, s_, A, B))
+
+
+def test_degenerate_ground_states_and_chunked_readback(Q):
+    """h = 0: z and its complement are both ground states (reading R11); the readback of
+    2^23 amplitudes crosses the 2^22-amplitude gather chunk."""
+    n = 23
+    _, J = inst.random_ising(n, 12)
+    h = np.zeros(n)
+    g, b = rand_angles(2, 12)
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        gs, emin, cnt = s.ground_states(max_out=8)
+        s.init_plus()
+        s.apply_qaoa(g, b)
+        psi = s.amplitudes()
+        ps = s.success_prob(gs)
+        en = s.energies()  # 2^23 energies cross the 2^23-energy probe chunk boundary exactly
+    assert cnt % 2 == 0 and all(((1 << n) - 1 - z) in gs for z in gs)
+    ref = o.qaoa_state(h, J, g, b)
+    assert_state_close(psi, ref)
+    assert abs(ps - o.success_prob(ref, gs)) <= 1e-9 * o.success_prob(ref, gs)
+    assert np.array_equal(en, o.energies(h, J))
+    assert np.array_equal(psi, psi[(1 << n) - 1 - np.arange(1 << n)])  # P5 at the GPU
+
+
+def test_set_ising_twice_and_reuse(Q):
+    n = 16
+    h1, J1 = inst.random_ising(n, 21)
+    h2, J2 = inst.random_ising(n, 22)
+    g, b = rand_angles(2, 23)
+    with Q.QSim(n) as s:
+        s.set_ising(h1, J1)
+        s.init_plus()
+        s.apply_qaoa(g, b)
+        s.set_ising(h2, J2)
+        s.init_plus()
+        s.apply_qaoa(g, b)
+        psi = s.amplitudes()
+        e = s.expect_hc()
+    ref = o.qaoa_state(h2, J2, g, b)
+    assert_state_close(psi, ref)
+    assert_expect_close(e, h2, J2, ref)
