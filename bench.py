@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--p", type=int, default=32)
     ap.add_argument("--nlocal", type=int, default=30, help="qubits per GPU shard (n = nlocal + log2 N)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+                    help="amplitude precision (fp64 = the north-star path; fp32 = the NEXT-4 mode)")
     return ap.parse_args()
 
 
@@ -201,7 +203,10 @@ def main():
     # recorded on it (torch's default stream is the legacy null stream, handle 0)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
-    sim = Q.QSim(n, rank=rank, world=world, nccl_unique_id=uid, cuda_stream=stream.cuda_stream)
+    f32 = args.precision == "fp32"
+    es = 8 if f32 else 16
+    sim = Q.QSim(n, rank=rank, world=world, nccl_unique_id=uid, cuda_stream=stream.cuda_stream,
+                 precision=Q.QSIM_FP32 if f32 else Q.QSIM_FP64)
     sim.set_ising(w["h"], w["J"])
 
     def step():
@@ -271,7 +276,7 @@ def main():
         achieved = avg_bytes / (avg_pass_ms / 1e3) / 1e9
         traffic = None
         tp = os.path.join(ROOT, "profiles", "pass_kernel_traffic.json")
-        if os.path.exists(tp):
+        if os.path.exists(tp) and not f32 and world == 1:
             try:
                 traffic = json.load(open(tp)).get("dram_bytes_per_launch")
             except Exception:
@@ -279,12 +284,13 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
             "config": {"workload": f"AQA exact-cover-shaped n={n} (N x 472, seed 0), p={p}, tau=0.4 ns, "
                                    f"DW-like schedule; step = |+> + {p} layers + <H_C> + P_success",
                        "n": n, "p": p, "n_local": args.nlocal, "parallelism": f"state sharded over {world} GPU"
                        + ("s (global-qubit swaps)" if world > 1 else ""),
-                       "l2": f"state {16 * (1 << args.nlocal) / 1e9:.1f} GB per GPU >> 126 MB L2 (no flush needed)"},
+                       "precision": args.precision,
+                       "l2": f"state {es * (1 << args.nlocal) / 1e9:.1f} GB per GPU >> 126 MB L2 (no flush needed)"},
             "sec_per_layer": ms_step / 1e3 / p,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -295,6 +301,14 @@ def main():
             "e2e": {"value": (1 << n) * p / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "sec_per_step": e2e_s},
             "gpu_launches": int(launches),
+            "nvlink": ({"swap_bytes_per_layer_per_dir": (world - 1) / world * es * (1 << args.nlocal),
+                        "layer_ms": ms_step / p,
+                        "implied_GBps_per_dir": (world - 1) / world * es * (1 << args.nlocal) / (ms_step / p / 1e3) / 1e9,
+                        "peak_GBps_per_dir": 770.0,
+                        "peak_source": "B200_PROFILING.md measured peer copy (nominal 900)",
+                        "note": "one global-qubit swap per layer, its stores spread over the layer's passes "
+                                "(split swap); implied rate = swap bytes / whole layer time"}
+                       if world > 1 else None),
             "clocks": clocks,
             "results": {"expect_hc": e, "p_success": ps, "r": w["r"]},
         }

@@ -51,16 +51,23 @@ enum {
     QSIM_ENOMEM = -2,      /* device memory capacity exceeded for 2^n amplitudes */
     QSIM_ERANGE = -3,      /* basis index out of [0, 2^n) */
     QSIM_ESTATE = -4,      /* qsim_set_ising not called yet */
-    QSIM_EUNSUPPORTED = -5,/* precision other than QSIM_FP64, or layout not supported */
+    QSIM_EUNSUPPORTED = -5,/* configuration not supported (e.g. QSIM_FP32 without the TMA kernel) */
     QSIM_ECUDA = -6,       /* CUDA runtime error (message in qsim_last_error) */
     QSIM_ENCCL = -7        /* NCCL error (multi-GPU handles) */
 };
 
-enum { QSIM_FP64 = 0, QSIM_FP32 = 1 /* reserved; returns QSIM_EUNSUPPORTED */ };
+/* Amplitude precision.  QSIM_FP64 is the north-star path (complex128 amplitudes).  QSIM_FP32
+ * (the precision of the paper's Table I GPU timings) stores
+ * complex64 amplitudes (8 bytes each, half the HBM traffic) and runs the butterflies and phase
+ * multiplications in FP32; energies E(z), tile fields and phase tables stay FP64 (E is still
+ * exact), reductions accumulate in FP64, and readback converts to FP64.  Error bound and
+ * tests: DESIGN.md §9. */
+enum { QSIM_FP64 = 0, QSIM_FP32 = 1 };
 
 /* Create a single-GPU handle on the current CUDA device for an n-qubit state
- * (1 <= n <= 40; the library allocates 16 * 2^n bytes of device memory, QSIM_ENOMEM
- * if that fails).  The state starts as |+>^n.  precision must be QSIM_FP64. */
+ * (1 <= n <= 40; the library allocates 16 * 2^n bytes of device memory (8 * 2^n for
+ * QSIM_FP32), QSIM_ENOMEM if that fails).  The state starts as |+>^n.  precision is
+ * QSIM_FP64 or QSIM_FP32 (else QSIM_EINVAL). */
 int qsim_create(int n, int precision, qsim_t **out);
 
 /* Multi-GPU / embedding variant.  The state is partitioned over `world` = 2^g ranks
@@ -190,6 +197,10 @@ int qsim_nccl_unique_id(void *out128);
  * last enable/read, then resets the counters. */
 int qsim_profile_enable(qsim_t *q, int on);
 int qsim_profile_read(qsim_t *q, double *ms_sum, uint64_t *count, double *bytes_sum);
+/* Per-pass variant: writes the duration (ms) of each recorded pass, in launch order, into
+ * ms_out[0 .. min(count, cap)) and returns the number of recorded passes (>= 0), or a negative
+ * error code; clears the record like qsim_profile_read.  Synchronises. */
+int qsim_profile_passes(qsim_t *q, double *ms_out, int cap);
 
 /* Diagnostic micro-benchmark (modifies the state): time `reps` back-to-back launches of
  * the tile pass over tile set `set` (0 = bits 0..11, 1.. = the run sets in ascending bit

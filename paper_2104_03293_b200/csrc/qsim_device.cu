@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(NTHR, 2) pass_kernel(const PassParams P) {
 }
 
 // ============================================================ standalone reduction (frame X)
+template <typename V>
 __global__ void __launch_bounds__(NTHR, 2) reduce_kernel(const PassParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CtaShared &cs = *reinterpret_cast<CtaShared *>(smem_raw + SmemLayout::tile);
@@ -183,11 +184,12 @@ __global__ void __launch_bounds__(NTHR, 2) reduce_kernel(const PassParams P) {
     __syncthreads();
     const u64 offX = thread_offset<FX>(P.L, lane, warp);
     double acc_e = 0.0, acc_n = 0.0;
-    double2 v[NR];
+    V v[NR];
+    const V *psi = reinterpret_cast<const V *>(P.psi);
     for (u64 ut = blockIdx.x; ut < P.ntiles; ut += gridDim.x) {
         const u64 tb = tile_base(P, ut);
-        prefetch_next(P, ut + gridDim.x, tid);
-        load_tile<FX>(v, P.psi + tb + offX, P.L);
+        if (sizeof(V) == 16) prefetch_next(P, ut + gridDim.x, tid);
+        load_tile<FX>(v, psi + tb + offX, P.L);
         accumulate<FX>(v, recs + ut, tX, fr, te, cs.eRR, acc_e, acc_n);
     }
     block_reduce2(cs, acc_e, acc_n, lane, warp, P.part + 2 * blockIdx.x);
@@ -210,16 +212,18 @@ __global__ void sum_partials_kernel(const double *part, int nparts, double *res)
 // The whole state lives in shared memory; all p layers run in one launch (config n=12
 // is launch-bound).  Phase: E(z) summed directly (exact for dyadic data),
 // then sincos; mixer: one butterfly sweep per qubit (eq:twocomponentupdates).
+template <typename V>
 __global__ void __launch_bounds__(512) small_kernel(const SmallParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *st = reinterpret_cast<double2 *>(smem_raw);
+    double2 *st = reinterpret_cast<double2 *>(smem_raw);  // FP64 working copy (FP32 states round on store)
+    V *psi = reinterpret_cast<V *>(P.psi);
     __shared__ double sh[KT];
     __shared__ double sJ[KT * KT];
     __shared__ double red[2][16];
     const int n = P.n, dim = 1 << n, tid = threadIdx.x, nt = blockDim.x;
     for (int i = tid; i < n; i += nt) sh[i] = P.hp[i];
     for (int i = tid; i < n * n; i += nt) sJ[i] = P.Jp[i];
-    for (int i = tid; i < dim; i += nt) st[i] = P.init ? make_double2(P.a0, 0.0) : P.psi[i];
+    for (int i = tid; i < dim; i += nt) st[i] = P.init ? make_double2(P.a0, 0.0) : dcast(psi[i]);
     __syncthreads();
     for (int k = 0; k < P.p; ++k) {
         const double g = P.ang[k], b = P.ang[P.p + k];
@@ -261,8 +265,9 @@ __global__ void __launch_bounds__(512) small_kernel(const SmallParams P) {
     }
     double acc_e = 0.0, acc_n = 0.0;
     for (int z = tid; z < dim; z += nt) {
-        const double2 a = st[z];
-        P.psi[z] = a;
+        const V av = vcast<V>(st[z]);
+        psi[z] = av;
+        const double2 a = dcast(av);
         if (P.reduce) {
             double e = 0.0;
             for (int i = 0; i < n; ++i) {
@@ -300,9 +305,10 @@ __global__ void __launch_bounds__(512) small_kernel(const SmallParams P) {
 }
 
 // ======================================================================== utilities
-__global__ void init_plus_kernel(double2 *psi, u64 count, double a0) {
+template <typename V>
+__global__ void init_plus_kernel(V *psi, u64 count, double a0) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x)
-        psi[i] = make_double2(a0, 0.0);
+        psi[i] = vcast<V>(make_double2(a0, 0.0));
 }
 
 // logical z -> physical full index via the permutation (pos[q] = physical bit of qubit q)
@@ -312,11 +318,12 @@ __device__ __forceinline__ u64 logical_to_physical(u64 z, const GatherParams &G)
     return x;
 }
 
-__global__ void gather_kernel(const GatherParams G, const double2 *psi, double2 *out) {
+template <typename V>
+__global__ void gather_kernel(const GatherParams G, const V *psi, double2 *out) {
     for (u64 k = blockIdx.x * (u64)blockDim.x + threadIdx.x; k < G.count; k += (u64)gridDim.x * blockDim.x) {
         const u64 z = G.list ? G.list[k] : G.first + k;
         const u64 x = logical_to_physical(z, G) ^ G.flip;
-        out[k] = ((x >> G.m) == G.rank) ? psi[x & ((1ull << G.m) - 1ull)] : make_double2(0.0, 0.0);
+        out[k] = ((x >> G.m) == G.rank) ? dcast(psi[x & ((1ull << G.m) - 1ull)]) : make_double2(0.0, 0.0);
     }
 }
 
@@ -341,10 +348,15 @@ cudaError_t setup_kernels() {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(pass_kernel<K_TURN_RUN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmemLayout::total);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(reduce_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)SmemLayout::total);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * TILE);
+    e = cudaFuncSetAttribute(reduce_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)SmemLayout::total);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(small_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * TILE);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(small_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * TILE);
 }
 
 cudaError_t launch_pass(const PassParams &P, int grid, cudaStream_t s) {
@@ -365,7 +377,8 @@ cudaError_t launch_tile_fields(const PassParams &P, void *rec, cudaStream_t s) {
 }
 
 cudaError_t launch_reduce(const PassParams &P, int grid, cudaStream_t s) {
-    reduce_kernel<<<grid, NTHR, SmemLayout::total, s>>>(P);
+    if (P.f32) reduce_kernel<float2><<<grid, NTHR, SmemLayout::total, s>>>(P);
+    else reduce_kernel<double2><<<grid, NTHR, SmemLayout::total, s>>>(P);
     return cudaGetLastError();
 }
 
@@ -375,17 +388,20 @@ cudaError_t launch_sum_partials(const double *part, int nparts, double *res, cud
 }
 
 cudaError_t launch_small(const SmallParams &P, cudaStream_t s) {
-    small_kernel<<<1, 512, (size_t)16 << P.n, s>>>(P);
+    if (P.f32) small_kernel<float2><<<1, 512, (size_t)16 << P.n, s>>>(P);
+    else small_kernel<double2><<<1, 512, (size_t)16 << P.n, s>>>(P);
     return cudaGetLastError();
 }
 
-cudaError_t launch_init_plus(double2 *psi, u64 count, double a0, int grid, cudaStream_t s) {
-    init_plus_kernel<<<grid, 256, 0, s>>>(psi, count, a0);
+cudaError_t launch_init_plus(double2 *psi, u64 count, double a0, int grid, cudaStream_t s, int f32) {
+    if (f32) init_plus_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<float2 *>(psi), count, a0);
+    else init_plus_kernel<<<grid, 256, 0, s>>>(psi, count, a0);
     return cudaGetLastError();
 }
 
-cudaError_t launch_gather(const GatherParams &G, const double2 *psi, double2 *out, int grid, cudaStream_t s) {
-    gather_kernel<<<grid, 256, 0, s>>>(G, psi, out);
+cudaError_t launch_gather(const GatherParams &G, const double2 *psi, double2 *out, int grid, cudaStream_t s, int f32) {
+    if (f32) gather_kernel<<<grid, 256, 0, s>>>(G, reinterpret_cast<const float2 *>(psi), out);
+    else gather_kernel<<<grid, 256, 0, s>>>(G, psi, out);
     return cudaGetLastError();
 }
 

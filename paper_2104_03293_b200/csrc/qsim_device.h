@@ -32,7 +32,9 @@ enum PassKind {
 
 struct PassParams {
     int kind;            // PassKind
-    double2 *psi;        // local shard, 2^m amplitudes
+    int f32;             // amplitude storage: 0 = FP64 (double2), 1 = FP32 (float2, NEXT-4 mode)
+    int multi;           // multi-GPU pass (swap stores / moving passes possible): MV kernel instances
+    double2 *psi;        // local shard, 2^m amplitudes (float2 * when f32; all state pointers alike)
     const double *hp;    // physical-frame fields, n
     const double *Jp;    // physical-frame couplings, n*n symmetric, zero diagonal
     int n, m;
@@ -59,6 +61,19 @@ struct PassParams {
     // dst[c][(rank << (m-g)) | y] (dst[c] = rank c's other state buffer, mapped over NVLink)
     int swap_store, gbits, rank;
     double2 *dst[8];
+    // split swap: the swap's data movement is shared by the passes of a layer.
+    // Group of an amplitude = bits [mv_pshift, mv_pshift + mv_pbits) of its local index (top-run
+    // bits below the swapped ones, never tile bits of the non-boundary sets).  A pass moves the
+    // amplitudes whose group lies in [mv_lo, mv_hi): mv == 2 (boundary pass, per element in
+    // store_tile_swapped), mv == 1 (other passes, whole tiles: tile at local (v | u), v != rank,
+    // is stored into rank v's other buffer at (rank | u)); everything else stays local, written
+    // out of place to dst[rank].
+    int mv, mv_pshift, mv_pbits;
+    unsigned mv_lo, mv_hi;
+    // tile visiting order: the CTA's k-th tile is rotl(k, ord_rot) over ord_bits tile-id bits,
+    // so that the tiles in flight at one time span all groups (moving passes interleave NVLink
+    // and HBM traffic instead of alternating phases of each); 0 = natural order
+    int ord_rot, ord_bits;
     int dbg;             // diagnostics (qsim_bench_pass): bit 0 skip stores, bit 1 skip state loads
     int tma_store;       // store tiles with TMA from the stage instead of STG from registers
     int l2hint;          // L2 cache policy: bits 0-1 loads, bits 2-3 stores (0 none, 1 evict_first, 2 evict_last)
@@ -77,6 +92,7 @@ struct PassParams {
 constexpr size_t TILE_REC_BYTES = 320;  // sizeof(TileRec)
 
 struct SmallParams {
+    int f32;             // FP32 state (float2 *) instead of FP64
     double2 *psi;
     const double *hp, *Jp;
     const double *ang;   // gamma[p], beta[p]
@@ -121,15 +137,18 @@ size_t pass_smem_bytes();
 size_t tma_smem_bytes();
 cudaError_t setup_tma_kernels();
 // TMA-pipelined pass (qsim_tma.cu); `tensor_map` points to a CUtensorMap (128 B)
-cudaError_t launch_tma_pass(const ::CUtensorMap_st &tensor_map, const PassParams &P, int grid, cudaStream_t s);
+// `store_map` is the tensor map of the output buffer (the same as `tensor_map` in place)
+cudaError_t launch_tma_pass(const ::CUtensorMap_st &tensor_map, const ::CUtensorMap_st &store_map,
+                            const PassParams &P, int grid, cudaStream_t s);
 cudaError_t setup_kernels();
 cudaError_t launch_pass(const PassParams &P, int grid, cudaStream_t s);
 cudaError_t launch_tile_fields(const PassParams &P, void *rec, cudaStream_t s);
 cudaError_t launch_reduce(const PassParams &P, int grid, cudaStream_t s);
 cudaError_t launch_sum_partials(const double *part, int nparts, double *res, cudaStream_t s);
 cudaError_t launch_small(const SmallParams &P, cudaStream_t s);
-cudaError_t launch_init_plus(double2 *psi, u64 count, double a0, int grid, cudaStream_t s);
-cudaError_t launch_gather(const GatherParams &G, const double2 *psi, double2 *out, int grid, cudaStream_t s);
+cudaError_t launch_init_plus(double2 *psi, u64 count, double a0, int grid, cudaStream_t s, int f32 = 0);
+cudaError_t launch_gather(const GatherParams &G, const double2 *psi, double2 *out, int grid, cudaStream_t s,
+                          int f32 = 0);
 cudaError_t launch_energy_probe(const GatherParams &G, const double *hp, const double *Jp,
                                 const ProbeSet &S, double *out, int grid, cudaStream_t s);
 

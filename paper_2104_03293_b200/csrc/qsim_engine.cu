@@ -54,9 +54,15 @@ struct PassOp {
     bool swap_after;  // multi-GPU: global-qubit swap (NCCL, in place) after this pass
     bool swap_fused;  // multi-GPU: this pass stores its output swapped into the peers' buffers
     int l1 = 0, l2 = 0;  // layer indices of mix1 / mix2 (general-mixer mode)
+    // split swap: share of the swap's data this pass moves (PassParams::mv, groups [lo, hi));
+    // swap_done marks the layer's last moving pass (the relabelling takes effect after it)
+    int mv = 0;
+    unsigned lo = 0, hi = 0;
+    bool swap_done = false;
 };
 
-TileSet make_set(int m, const std::vector<int> &Lpos, unsigned own) {
+// es = bytes per amplitude (16 FP64, 8 FP32)
+TileSet make_set(int m, const std::vector<int> &Lpos, unsigned own, int es = 16) {
     TileSet S{};
     u64 lm = 0;
     for (int i = 0; i < qk::KT; ++i) {
@@ -98,7 +104,7 @@ TileSet make_set(int m, const std::vector<int> &Lpos, unsigned own) {
             else take = len;
             const cuuint64_t sz = 1ull << take;
             S.tm_dim[d] = (d == 0) ? 2 * sz : sz;
-            S.tm_stride[d] = 16ull << pos;
+            S.tm_stride[d] = (cuuint64_t)es << pos;
             S.tm_box[d] = tile ? (cuuint32_t)S.tm_dim[d] : 1u;
             S.tm_clen[d] = tile ? 0 : take;
             S.tm_cshift[d] = tile ? 0 : ubit;
@@ -113,7 +119,7 @@ TileSet make_set(int m, const std::vector<int> &Lpos, unsigned own) {
     // pad to 5 dims (the kernel always issues the .5d form of cp.async.bulk.tensor)
     for (int d = S.tm_rank; d < 5; ++d) {
         S.tm_dim[d] = 1;
-        S.tm_stride[d] = 16ull << m;  // past the end of the shard; dim size 1
+        S.tm_stride[d] = (cuuint64_t)es << m;  // past the end of the shard; dim size 1
         S.tm_box[d] = 1;
         S.tm_clen[d] = 0;
         S.tm_cshift[d] = 0;
@@ -121,14 +127,15 @@ TileSet make_set(int m, const std::vector<int> &Lpos, unsigned own) {
     return S;
 }
 
-// Tile sets over m >= 13 local bits: S_0 = bits 0..11 (all mixed); then runs of <= 9
+// Tile sets over m >= 13 local bits: S_0 = bits 0..11 (all mixed); then runs of <= 12 - minpass
 // mixed bits taken top-down from bit m-1, each completed to 12 tile bits with the
-// lowest bits as unmixed "passengers" (>= 3 of them -> >= 128-byte coalesced runs).
-std::vector<TileSet> build_sets(int m) {
+// lowest bits as unmixed "passengers" (>= minpass of them: 3 -> >= 128-byte coalesced rows in
+// FP64, 64-byte rows in FP32 unless minpass = 4).
+std::vector<TileSet> build_sets(int m, int es = 16, int minpass = 3) {
     std::vector<std::pair<int, int>> runs;  // [a, a+len)
     int end = m;
     while (end > qk::KT) {
-        int len = std::min(9, end - qk::KT);
+        int len = std::min(qk::KT - minpass, end - qk::KT);
         runs.push_back({end - len, len});
         end -= len;
     }
@@ -136,14 +143,14 @@ std::vector<TileSet> build_sets(int m) {
     std::vector<TileSet> sets;
     std::vector<int> L0(qk::KT);
     for (int i = 0; i < qk::KT; ++i) L0[i] = i;
-    sets.push_back(make_set(m, L0, (1u << qk::KT) - 1));
+    sets.push_back(make_set(m, L0, (1u << qk::KT) - 1, es));
     sets.back().full12 = true;
     for (auto &r : runs) {
         std::vector<int> L;
         int npass = qk::KT - r.second;
         for (int i = 0; i < npass; ++i) L.push_back(i);
         for (int i = 0; i < r.second; ++i) L.push_back(r.first + i);
-        sets.push_back(make_set(m, L, ((1u << r.second) - 1) << npass));
+        sets.push_back(make_set(m, L, ((1u << r.second) - 1) << npass, es));
         sets.back().full12 = false;
     }
     return sets;
@@ -156,8 +163,15 @@ std::vector<TileSet> build_sets(int m) {
 // (P-1) p + 1 passes.  G > 1: fixed schedule, top run first (boundary pass: arrivals
 // with beta_{k-1}, phase_k, set with beta_k), the other sets, then the swap of the top
 // g local bits with the global bits: P p + 1 passes, p swaps.
+// `split` (fused swap only): the share of the swap's amplitude groups each pass of the layer
+// moves (weights per pass, boundary pass first; empty = the boundary pass moves everything).
+struct SwapSplit {
+    int ngroups = 1;             // 2^mv_pbits
+    std::vector<double> weights; // per pass of the layer, boundary pass first
+};
+
 std::vector<PassOp> build_schedule(int nsets, int g, int p, const double *gam, const double *bet,
-                                   bool first_init, bool fused = false) {
+                                   bool first_init, bool fused = false, const SwapSplit *split = nullptr) {
     std::vector<PassOp> ops;
     const int P = nsets;
     if (g == 0) {
@@ -180,19 +194,50 @@ std::vector<PassOp> build_schedule(int nsets, int g, int p, const double *gam, c
         // G > 1: per layer the boundary pass on the top run (arrivals of the last swap get
         // beta_{k-1}, phase_k, the set gets beta_k), then the other sets with beta_k.  The swap
         // of the top g local bits with the global bits either rides on the boundary pass's
-        // stores (fused: output written straight into the peers' second buffers over NVLink)
-        // or follows the layer's last pass (NCCL, in place).  The trailing pass gives the last
-        // arrivals beta_{p-1}.
+        // stores (fused: output written straight into the peers' second buffers over NVLink;
+        // with `split` the data movement is shared by all passes of the layer, each moving whole
+        // groups of amplitudes) or follows the layer's last pass (NCCL, in place).  The trailing
+        // pass gives the last arrivals beta_{p-1}.
         const int top = P - 1;
         const unsigned arrivals = ((1u << g) - 1) << (qk::KT - g);  // top g tile bits of the top set
+        // group ranges [b_i, b_{i+1}) per pass of the layer
+        std::vector<unsigned> bnd(P + 1, 0u);
+        const int ng = (fused && split && (int)split->weights.size() == P) ? split->ngroups : 1;
+        if (ng > 1) {
+            double tot = 0.0;
+            for (double w : split->weights) tot += w;
+            double acc = 0.0;
+            for (int i = 0; i < P; ++i) {
+                acc += split->weights[i];
+                bnd[i + 1] = (unsigned)std::lround(acc / tot * ng);
+            }
+            bnd[P] = (unsigned)ng;
+        } else {
+            for (int i = 1; i <= P; ++i) bnd[i] = 1u;
+        }
         for (int k = 0; k < p; ++k) {
+            const size_t first = ops.size();
             if (k == 0)
                 ops.push_back({top, first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false, fused, 0, 0});
             else
                 ops.push_back({top, false, true, false, arrivals, ~0u, bet[k - 1], bet[k], gam[k], false, fused, k - 1, k});
             for (int s = P - 2; s >= 0; --s)
                 ops.push_back({s, false, false, false, ~0u, 0u, bet[k], 0.0, 0.0, false, false, k, 0});
-            if (!fused) ops.back().swap_after = true;
+            if (!fused) {
+                ops.back().swap_after = true;
+                continue;
+            }
+            // a pass with a non-empty group range moves (out of place): the boundary pass per
+            // element (mv 2), the others whole tiles (mv 1); the rest run in place
+            size_t last = first;
+            for (int i = 0; i < P; ++i) {
+                PassOp &o = ops[first + i];
+                o.lo = bnd[i];
+                o.hi = bnd[i + 1];
+                o.mv = (o.hi > o.lo) ? (i == 0 ? 2 : 1) : 0;
+                if (o.mv) last = first + i;
+            }
+            ops[last].swap_done = true;
         }
         ops.push_back({top, false, false, false, arrivals, 0u, bet[p - 1], 0.0, 0.0, false, false, p - 1, 0});
     }
@@ -240,6 +285,8 @@ int ilog2(int w) {
 
 struct qsim {
     int n = 0, m = 0, g = 0, rank = 0, world = 1;
+    int f32 = 0;        // QSIM_FP32: float2 amplitudes (NEXT-4 precision mode)
+    size_t es = 16;     // bytes per amplitude
     int dev = 0, num_sms = 148;
     double2 *psi = nullptr;
     bool own_psi = false;
@@ -247,6 +294,12 @@ struct qsim {
     void *user_buf = nullptr; // caller-owned state storage (never freed here)
     // fused swap: both state buffers of every rank mapped through CUDA IPC
     bool fused_swap = false;
+    // split swap (QSIM_SPLIT_SWAP, default on): the passes of a layer share the swap's NVLink
+    // traffic; groups = local bits [mv_pshift, mv_pshift + mv_pbits) (the top run below the
+    // swapped bits); per-pass weights QSIM_SPLIT_W ("boundary,next,...")
+    bool split = false;
+    int mv_pshift = 0, mv_pbits = 0;
+    std::vector<double> split_w;
     int cur = 0;                       // which of bufs[] currently holds the state
     double2 *bufs[2] = {nullptr, nullptr};
     double2 *peer[2][8] = {};          // peer[b][c] = rank c's buffer b (own buffer for c == rank)
@@ -382,7 +435,7 @@ int scratch(qsim *q, size_t bytes) {
 int materialize_plus(qsim *q) {
     if (!q->pending_plus) return QSIM_OK;
     double a0 = std::pow(2.0, -0.5 * q->n);
-    CK(qk::launch_init_plus(q->psi, 1ull << q->m, a0, q->num_sms * 8, q->st));
+    CK(qk::launch_init_plus(q->psi, 1ull << q->m, a0, q->num_sms * 8, q->st, q->f32));
     q->launches++;
     q->pending_plus = false;
     reset_perm(q);  // |+>^n is invariant under qubit relabelling
@@ -392,6 +445,8 @@ int materialize_plus(qsim *q) {
 
 qk::PassParams base_params(qsim *q, const TileSet &S) {
     qk::PassParams P{};
+    P.f32 = q->f32;
+    P.multi = q->fused_swap ? 1 : 0;
     P.psi = q->psi;
     P.hp = q->cur_hp;
     P.Jp = q->cur_Jp;
@@ -430,22 +485,27 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 }
 
 // launch one pass: TMA-pipelined kernel (one CTA per SM) or the register-direct kernel
-int launch_pass_any(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out) {
+// `out`: output buffer of an out-of-place pass (TMA stores go there), nullptr = in place
+int launch_pass_any(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, double2 *out = nullptr) {
     if (q->use_tma) {
         auto enc = tmap_encoder();
         if (!enc) return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled unavailable");
-        CUtensorMap tm;
+        CUtensorMap tm[2];
         cuuint32_t es[5] = {1, 1, 1, 1, 1};
-        CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5u, (void *)q->psi, S.tm_dim,
-                         S.tm_stride + 1, S.tm_box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         (CUtensorMapL2promotion)q->l2promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+        const CUtensorMapDataType dt = q->f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+        for (int k = 0; k < (out ? 2 : 1); ++k) {
+            CUresult r = enc(&tm[k], dt, 5u, (void *)(k ? out : q->psi), S.tm_dim,
+                             S.tm_stride + 1, S.tm_box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             (CUtensorMapL2promotion)q->l2promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS)
+                return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+        }
         for (int d = 0; d < 5; ++d) {
             P.tm_clen[d] = S.tm_clen[d];
             P.tm_cshift[d] = S.tm_cshift[d];
         }
         int grid = (int)std::min<u64>((u64)q->num_sms, S.ntiles);
-        CK(qk::launch_tma_pass(tm, P, grid, q->st));
+        CK(qk::launch_tma_pass(tm[0], out ? tm[1] : tm[0], P, grid, q->st));
         *grid_out = grid;
     } else {
         int grid = grid_for(q, S.ntiles);
@@ -471,14 +531,15 @@ void swap_bookkeeping(qsim *q) {
     relabel(q, newp);
 }
 
-// after a fused swap pass: wait until every rank's pass (and its NVLink stores) is done, then
-// the other buffer holds the state
-int finish_fused_swap(qsim *q) {
+// after a moving pass of the fused swap: wait until every rank's pass (and its NVLink stores)
+// is done, then the other buffer holds the state; after the layer's last moving pass the
+// relabelling takes effect
+int finish_fused_swap(qsim *q, bool done) {
     NK(ncclAllReduce(q->d_bar, q->d_bar, 1, ncclDouble, ncclSum, q->comm, q->st));
     q->cur ^= 1;
     q->psi = q->bufs[q->cur];
     q->tmp = q->bufs[q->cur ^ 1];
-    swap_bookkeeping(q);
+    if (done) swap_bookkeeping(q);
     return QSIM_OK;
 }
 
@@ -487,16 +548,18 @@ int do_swap(qsim *q) {
     const int G = q->world;
     swap_bookkeeping(q);
     const u64 chunk = 1ull << (q->m - q->g);  // amplitudes per chunk
-    const size_t cbytes = chunk * sizeof(double2);
+    const size_t cbytes = chunk * q->es;
+    const size_t cdbl = cbytes / 8;           // chunk in doubles (NCCL count)
+    auto at = [&](double2 *b, u64 amp) { return (double2 *)((char *)b + amp * q->es); };
     if (q->tmp) {
         NK(ncclGroupStart());
         for (int c = 0; c < G; ++c) {
             if (c == q->rank) continue;
-            NK(ncclSend(q->psi + c * chunk, chunk * 2, ncclDouble, c, q->comm, q->st));
-            NK(ncclRecv(q->tmp + c * chunk, chunk * 2, ncclDouble, c, q->comm, q->st));
+            NK(ncclSend(at(q->psi, c * chunk), cdbl, ncclDouble, c, q->comm, q->st));
+            NK(ncclRecv(at(q->tmp, c * chunk), cdbl, ncclDouble, c, q->comm, q->st));
         }
         NK(ncclGroupEnd());
-        CK(cudaMemcpyAsync(q->tmp + q->rank * chunk, q->psi + q->rank * chunk, cbytes,
+        CK(cudaMemcpyAsync(at(q->tmp, q->rank * chunk), at(q->psi, q->rank * chunk), cbytes,
                            cudaMemcpyDeviceToDevice, q->st));
         std::swap(q->psi, q->tmp);
         if (q->fused_swap) q->cur ^= 1;
@@ -504,14 +567,14 @@ int do_swap(qsim *q) {
         // in place through a bounded staging ring: piece by piece, copy the outgoing
         // piece of every peer chunk to staging, then send it and receive in place
         u64 piece = std::min<u64>(chunk, 1ull << 26);  // 1 GiB per peer
-        int rc = scratch(q, (size_t)(G - 1) * piece * sizeof(double2));
+        int rc = scratch(q, (size_t)(G - 1) * piece * q->es);
         if (rc) return rc;
         double2 *stg = (double2 *)q->d_scratch;
         for (u64 off = 0; off < chunk; off += piece) {
             int slot = 0;
             for (int c = 0; c < G; ++c) {
                 if (c == q->rank) continue;
-                CK(cudaMemcpyAsync(stg + (size_t)slot * piece, q->psi + c * chunk + off, piece * sizeof(double2),
+                CK(cudaMemcpyAsync(at(stg, (u64)slot * piece), at(q->psi, c * chunk + off), piece * q->es,
                                    cudaMemcpyDeviceToDevice, q->st));
                 ++slot;
             }
@@ -519,8 +582,8 @@ int do_swap(qsim *q) {
             slot = 0;
             for (int c = 0; c < G; ++c) {
                 if (c == q->rank) continue;
-                NK(ncclSend(stg + (size_t)slot * piece, piece * 2, ncclDouble, c, q->comm, q->st));
-                NK(ncclRecv(q->psi + c * chunk + off, piece * 2, ncclDouble, c, q->comm, q->st));
+                NK(ncclSend(at(stg, (u64)slot * piece), piece * q->es / 8, ncclDouble, c, q->comm, q->st));
+                NK(ncclRecv(at(q->psi, c * chunk + off), piece * q->es / 8, ncclDouble, c, q->comm, q->st));
                 ++slot;
             }
             NK(ncclGroupEnd());
@@ -590,6 +653,7 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         std::copy(bet, bet + p, ang.begin() + p);
         CK(cudaMemcpyAsync(q->d_ang, ang.data(), sizeof(double) * 2 * p, cudaMemcpyHostToDevice, q->st));
         qk::SmallParams S{};
+        S.f32 = q->f32;
         S.psi = q->psi;
         S.hp = q->cur_hp;
         S.Jp = q->cur_Jp;
@@ -616,7 +680,13 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         q->res_valid = !q->gmats;
         return QSIM_OK;
     }
-    std::vector<PassOp> ops = build_schedule((int)q->sets.size(), q->g, p, gam, bet, q->pending_plus, q->fused_swap);
+    SwapSplit sp;
+    if (q->split) {
+        sp.ngroups = 1 << q->mv_pbits;
+        sp.weights = q->split_w;
+    }
+    std::vector<PassOp> ops = build_schedule((int)q->sets.size(), q->g, p, gam, bet, q->pending_plus, q->fused_swap,
+                                             q->split ? &sp : nullptr);
     int last_grid = 0;
     for (const PassOp &op : ops) {
         const TileSet &S = q->sets[op.set];
@@ -652,11 +722,24 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         P.reduce = op.reduce;
         P.gamma = op.gamma;
         P.rec = q->d_rec;
-        if (op.swap_fused) {
-            P.swap_store = 1;
+        double2 *outbuf = nullptr;  // out-of-place output (moving passes of the fused swap)
+        if (op.mv) {
+            P.swap_store = op.mv == 2;
+            P.mv = op.mv;
             P.gbits = q->g;
             P.rank = q->rank;
+            P.mv_pshift = q->mv_pshift;
+            P.mv_pbits = q->split ? q->mv_pbits : 0;
+            P.mv_lo = op.lo;
+            P.mv_hi = op.hi;
             for (int c = 0; c < q->world; ++c) P.dst[c] = q->peer[q->cur ^ 1][c];
+            outbuf = q->bufs[q->cur ^ 1];
+            if (op.mv == 1 && P.mv_pbits > 0) {
+                // visit the tiles group bits first (the group bits sit above all 12 tile bits of
+                // a non-boundary set, so they are tile-id bits mv_pshift - 12 ..)
+                P.ord_bits = q->m - qk::KT;
+                P.ord_rot = (q->mv_pshift - qk::KT) % P.ord_bits;
+            }
         }
         if (op.phase || op.reduce) {
             CK(qk::launch_tile_fields(P, q->d_rec, q->st));
@@ -670,17 +753,17 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
             CK(cudaEventRecord(e0, q->st));
         }
         {
-            int rc = launch_pass_any(q, S, P, &grid);
+            int rc = launch_pass_any(q, S, P, &grid, outbuf);
             if (rc) return rc;
         }
         if (q->prof) {
             CK(cudaEventRecord(e1, q->st));
             // algorithmic HBM bytes: read + write of the shard, write only for the init pass
-            q->prof_bytes.push_back((op.init ? 16.0 : 32.0) * (double)(1ull << q->m));
+            q->prof_bytes.push_back((op.init ? 1.0 : 2.0) * (double)q->es * (double)(1ull << q->m));
         }
         last_grid = grid;
-        if (op.swap_fused) {
-            int rc = finish_fused_swap(q);
+        if (op.mv) {
+            int rc = finish_fused_swap(q, op.swap_done);
             if (rc) return rc;
         }
         if (op.swap_after) {
@@ -852,6 +935,7 @@ int run_reduce(qsim *q) {
     if (q->res_valid) return QSIM_OK;
     if (q->m <= qk::KT) {
         qk::SmallParams S{};
+        S.f32 = q->f32;
         S.psi = q->psi;
         S.hp = q->cur_hp;
         S.Jp = q->cur_Jp;
@@ -908,7 +992,7 @@ int gather_host(qsim *q, u64 first, u64 count, const uint64_t *hlist, double *ou
             CK(cudaMemcpyAsync(dlist, hlist + done, c * sizeof(u64), cudaMemcpyHostToDevice, q->st));
         }
         qk::GatherParams G = gather_params(q, first + done, c, dlist);
-        CK(qk::launch_gather(G, q->psi, dout, (int)std::min<u64>((c + 255) / 256, 4096), q->st));
+        CK(qk::launch_gather(G, q->psi, dout, (int)std::min<u64>((c + 255) / 256, 4096), q->st, q->f32));
         q->launches++;
         if (q->world > 1) NK(ncclAllReduce(dout, dout, c * 2, ncclDouble, ncclSum, q->comm, q->st));
         CK(cudaMemcpyAsync(out + 2 * done, dout, c * sizeof(double2), cudaMemcpyDeviceToHost, q->st));
@@ -919,7 +1003,9 @@ int gather_host(qsim *q, u64 first, u64 count, const uint64_t *hlist, double *ou
 
 int create_common(qsim *q, int n, int precision, int rank, int world, const void *uid, void *buf,
                   size_t buf_bytes, void *stream) {
-    if (precision != QSIM_FP64) return fail(q, QSIM_EUNSUPPORTED, "only QSIM_FP64 is supported");
+    if (precision != QSIM_FP64 && precision != QSIM_FP32) return fail(q, QSIM_EINVAL, "unknown precision");
+    q->f32 = precision == QSIM_FP32;
+    q->es = q->f32 ? 8 : 16;
     if (n < 1 || n > qk::NMAX) return fail(q, QSIM_EINVAL, "n out of range [1, 40]");
     int g = ilog2(world);
     if (world < 1 || world > 8 || g < 0) return fail(q, QSIM_EINVAL, "world must be 1, 2, 4 or 8");
@@ -939,7 +1025,7 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
         CK(cudaStreamCreateWithFlags(&q->st, cudaStreamNonBlocking));
         q->own_stream = true;
     }
-    const size_t bytes = (size_t)16 << q->m;
+    const size_t bytes = q->es << q->m;
     if (buf) {
         if (buf_bytes < bytes) return fail(q, QSIM_EINVAL, "state_buf too small");
         q->psi = (double2 *)buf;
@@ -959,11 +1045,13 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     CK(cudaMalloc(&q->d_part, sizeof(double) * 2 * 4 * q->num_sms));
     CK(cudaMalloc(&q->d_res, sizeof(double) * 2));
     if (q->m > qk::KT) {
-        q->sets = build_sets(q->m);
+        int minpass = 3;
+        if (const char *e = std::getenv("QSIM_F32_PASSENGERS"); q->f32 && e) minpass = std::max(3, std::min(6, std::atoi(e)));
+        q->sets = build_sets(q->m, (int)q->es, minpass);
         CK(cudaMalloc(&q->d_rec, qk::TILE_REC_BYTES << (q->m - qk::KT)));
     }
     if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
-    if (world == 1 && q->m >= qk::KT + 9 && q->use_tma && !buf) {
+    if (world == 1 && q->m >= qk::KT + 9 && q->use_tma && !buf && !q->f32) {
         // relabelling schedule: needs a second buffer (kept only if >= 8 GiB stay free)
         // (measured slower than the in-place schedule on B200: concurrent scattered reads and
         // contiguous writes stream at ~84 % while either alone runs at ~98 %; opt-in only)
@@ -1035,6 +1123,36 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
                 }
             q->fused_swap = true;
             q->cur = 0;
+            // split swap: groups from the top run's bits below the swapped ones
+            const TileSet &T = q->sets.back();
+            int a_top = q->m;
+            for (int i = 0; i < qk::KT; ++i)
+                if ((T.own >> i) & 1u) a_top = std::min(a_top, T.L[i]);
+            const char *sz = std::getenv("QSIM_SPLIT_SWAP");
+            q->mv_pshift = a_top;
+            q->mv_pbits = std::min(10, std::max(0, q->m - q->g - a_top));
+            q->split = q->mv_pbits > 0 && q->sets.size() > 1 && !(sz && std::atoi(sz) == 0);
+            // default weights ~ the passes' measured single-GPU times (boundary turning run,
+            // plain runs, the 12-bit set)
+            // (measured on 2 B200s: a non-boundary pass moves its share at almost no cost when
+            // the moving tiles are interleaved with local ones, while the boundary pass pays
+            // ~1.7 ms for its per-element STG stores whatever its share: at G = 2 it moves
+            // nothing and keeps its TMA stores in place)
+            q->split_w.clear();
+            q->split_w.push_back(world == 2 ? 0.0 : 1.0);
+            for (int s2 = (int)q->sets.size() - 2; s2 >= 0; --s2) q->split_w.push_back(1.0);
+            if (const char *w = std::getenv("QSIM_SPLIT_W")) {
+                std::vector<double> ws;
+                const char *c = w;
+                while (*c) {
+                    char *e = nullptr;
+                    double v = std::strtod(c, &e);
+                    if (e == c) break;
+                    ws.push_back(v);
+                    c = (*e == ',') ? e + 1 : e;
+                }
+                if (ws.size() == q->sets.size()) q->split_w = ws;
+            }
         }
     }
     q->pending_plus = true;
@@ -1048,6 +1166,8 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
         for (const TileSet &S : q->sets)
             if (!S.tm_ok) q->use_tma = 0;
     }
+    if (q->f32 && !q->use_tma && q->m > qk::KT)
+        return fail(q, QSIM_EUNSUPPORTED, "QSIM_FP32 needs the TMA pass kernel");
     return QSIM_OK;
 }
 
@@ -1643,11 +1763,25 @@ int qsim_profile_read(qsim_t *q, double *ms_sum, uint64_t *count, double *bytes_
     return QSIM_OK;
 }
 
+int qsim_profile_passes(qsim_t *q, double *ms_out, int cap) {
+    if (!q || (cap > 0 && !ms_out)) return QSIM_EINVAL;
+    CK(cudaStreamSynchronize(q->st));
+    const int npass = (int)(q->ev_used / 2);
+    for (int i = 0; i < npass && i < cap; ++i) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, q->ev_pool[2 * i], q->ev_pool[2 * i + 1]));
+        ms_out[i] = t;
+    }
+    q->ev_used = 0;
+    q->prof_bytes.clear();
+    return npass;
+}
+
 uint64_t qsim_kernel_launches(const qsim_t *q) { return q ? q->launches : 0; }
 
 const char *qsim_last_error(const qsim_t *q) { return q ? q->err.c_str() : g_create_error.c_str(); }
 
-const char *qsim_version(void) { return "qsim-b200 0.1 (sm_100a, FP64)"; }
+const char *qsim_version(void) { return "qsim-b200 0.2 (sm_100a, FP64 + FP32 mode)"; }
 
 int qsim_nccl_unique_id(void *out128) {
     if (!out128) return QSIM_EINVAL;

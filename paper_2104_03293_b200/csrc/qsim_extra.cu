@@ -13,6 +13,7 @@ namespace qk {
 
 // ---------------------------------------------------------------------------------- NEXT-2
 // per CTA: vec[x] = sum over its tiles of sum_z |psi_z|^2 s_x(z ^ F) for physical bit x
+template <typename V>
 __global__ void __launch_bounds__(NTHR, 1) spin_kernel(const PassParams P, double *part) {
     __shared__ double red[NTHR / 32][NMAX + KT];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -29,14 +30,16 @@ __global__ void __launch_bounds__(NTHR, 1) spin_kernel(const PassParams P, doubl
     for (int x = 0; x < NMAX; ++x) acc[x] = 0.0;
 #pragma unroll
     for (int t = 0; t < KT; ++t) acct[t] = 0.0;
-    double2 v[NR];
+    V v[NR];
+    const V *psi = reinterpret_cast<const V *>(P.psi);
     for (u64 ut = blockIdx.x; ut < P.ntiles; ut += gridDim.x) {
         const u64 tb = tile_base(P, ut);
-        load_tile<FX>(v, P.psi + tb + offX, P.L);
+        load_tile<FX>(v, psi + tb + offX, P.L);
         double Pt = 0.0, Sr[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
-            const double p = fma(v[j].x, v[j].x, v[j].y * v[j].y);
+            const double2 a = dcast(v[j]);
+            const double p = fma(a.x, a.x, a.y * a.y);
             Pt += p;
 #pragma unroll
             for (int r = 0; r < 5; ++r) Sr[r] += ((j >> r) & 1) ? p : -p;
@@ -169,7 +172,8 @@ __global__ void min_partials_kernel(const double *part, int nparts, double *res)
 }
 
 cudaError_t launch_spin(const PassParams &P, double *part, int grid, cudaStream_t s) {
-    spin_kernel<<<grid, NTHR, 0, s>>>(P, part);
+    if (P.f32) spin_kernel<float2><<<grid, NTHR, 0, s>>>(P, part);
+    else spin_kernel<double2><<<grid, NTHR, 0, s>>>(P, part);
     return cudaGetLastError();
 }
 cudaError_t launch_sum_vec(const double *part, int nparts, int n, double *out, cudaStream_t s) {

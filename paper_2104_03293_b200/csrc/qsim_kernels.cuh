@@ -31,8 +31,25 @@ namespace qk {
 // ------------------------------------------------------------------------------ helpers
 __device__ __forceinline__ double spin(u64 x, int j) { return ((x >> j) & 1ull) ? 1.0 : -1.0; }
 
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(fma(a.x, b.x, -(a.y * b.y)), fma(a.x, b.y, a.y * b.x));
+// amplitude storage types: FP64 (double2, the north-star precision) or FP32 (float2, the
+// NEXT-4 precision mode).  Energies, fields and phase tables are always FP64.
+template <typename V> struct VT;
+template <> struct VT<double2> {
+    typedef double S;
+    __device__ static double2 mk(double a, double b) { return make_double2(a, b); }
+};
+template <> struct VT<float2> {
+    typedef float S;
+    __device__ static float2 mk(float a, float b) { return make_float2(a, b); }
+};
+template <typename V> __device__ __forceinline__ V vcast(double2 a) {
+    return VT<V>::mk((typename VT<V>::S)a.x, (typename VT<V>::S)a.y);
+}
+template <typename V> __device__ __forceinline__ double2 dcast(V a) { return make_double2((double)a.x, (double)a.y); }
+
+template <typename V>
+__device__ __forceinline__ V cmul(V a, V b) {
+    return VT<V>::mk(fma(a.x, b.x, -(a.y * b.y)), fma(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ double2 conjd(double2 a) { return make_double2(a.x, -a.y); }
 
@@ -115,26 +132,38 @@ template <> struct Frame<FW> {
     }
 };
 
+// Lane skew of a frame's register slots in linear shared memory (element t at t * sizeof(V)):
+// slot j of a lane holds register pattern j ^ skew.  FP64 (16 B, 8 lanes per wavefront):
+// frame Y (lanes on t5..t9) skews t0..t2.  FP32 (8 B, 16 lanes per wavefront): Y skews t0..t3;
+// W (lanes t0,t1,t2,t8,t9) skews t3 by lane bit 3 (t8), so each half-warp covers 32 banks.
+template <int F, typename V>
+__device__ __forceinline__ int frame_skew(int lane) {
+    if (sizeof(V) == 16) return F == FY ? (lane & 7) : 0;
+    return F == FY ? (lane & 15) : (F == FW ? ((lane >> 3) & 1) : 0);
+}
+
 // ------------------------------------------------------------------------- butterflies
 // (a, b) <- (a - i t b, b - i t a) = e^{-i beta X} / cos(beta) with t = tan(beta).
 // For |tan beta| > 1 the host uses e^{-i beta X} = (-i X) e^{-i (beta - pi/2) X}
 // (t = -cot beta, kappa = -i sin beta): the X gates commute with every mixer and are
 // tracked as an index flip mask F (state holds psi_{x xor F} at physical index x), so
 // there is one butterfly form and no data movement for them.
-template <int RBIT>
-__device__ __forceinline__ void bfly(double2 (&v)[NR], double t) {
+template <int RBIT, typename V>
+__device__ __forceinline__ void bfly(V (&v)[NR], double td) {
+    typedef typename VT<V>::S S;
+    const S t = (S)td;
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
         if (j & (1 << RBIT)) continue;
-        const double2 a = v[j], b = v[j | (1 << RBIT)];
-        v[j] = make_double2(fma(t, b.y, a.x), fma(-t, b.x, a.y));
-        v[j | (1 << RBIT)] = make_double2(fma(t, a.y, b.x), fma(-t, a.x, b.y));
+        const V a = v[j], b = v[j | (1 << RBIT)];
+        v[j] = VT<V>::mk(fma(t, b.y, a.x), fma(-t, b.x, a.y));
+        v[j | (1 << RBIT)] = VT<V>::mk(fma(t, a.y, b.x), fma(-t, a.x, b.y));
     }
 }
 
 // mix the tile bits of `mask` that are register bits of frame F
-template <int F>
-__device__ __forceinline__ void mix_frame(double2 (&v)[NR], unsigned mask, double t) {
+template <int F, typename V>
+__device__ __forceinline__ void mix_frame(V (&v)[NR], unsigned mask, double t) {
     const unsigned m5 = (mask >> Frame<F>::RB) & 0x1Fu;
     if (m5 & 1) bfly<0>(v, t);
     if (m5 & 2) bfly<1>(v, t);
@@ -144,49 +173,51 @@ __device__ __forceinline__ void mix_frame(double2 (&v)[NR], unsigned mask, doubl
 }
 
 // general 2x2 butterfly: (a, b) <- (m00 a + m01 b, m10 a + m11 b)
-__device__ __forceinline__ double2 cmac(double2 m, double2 x, double2 acc) {
-    return make_double2(fma(m.x, x.x, fma(-m.y, x.y, acc.x)), fma(m.x, x.y, fma(m.y, x.x, acc.y)));
+template <typename V>
+__device__ __forceinline__ V cmac(V m, V x, V acc) {
+    return VT<V>::mk(fma(m.x, x.x, fma(-m.y, x.y, acc.x)), fma(m.x, x.y, fma(m.y, x.x, acc.y)));
 }
-template <int RBIT>
-__device__ __forceinline__ void gbfly(double2 (&v)[NR], const double2 (&M)[4]) {
-    const double2 m00 = M[0], m01 = M[1], m10 = M[2], m11 = M[3];
+template <int RBIT, typename V>
+__device__ __forceinline__ void gbfly(V (&v)[NR], const double2 (&M)[4]) {
+    const V m00 = vcast<V>(M[0]), m01 = vcast<V>(M[1]), m10 = vcast<V>(M[2]), m11 = vcast<V>(M[3]);
+    const V zero = VT<V>::mk(0, 0);
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
         if (j & (1 << RBIT)) continue;
-        const double2 a = v[j], b = v[j | (1 << RBIT)];
-        v[j] = cmac(m00, a, cmac(m01, b, make_double2(0.0, 0.0)));
-        v[j | (1 << RBIT)] = cmac(m10, a, cmac(m11, b, make_double2(0.0, 0.0)));
+        const V a = v[j], b = v[j | (1 << RBIT)];
+        v[j] = cmac(m00, a, cmac(m01, b, zero));
+        v[j | (1 << RBIT)] = cmac(m10, a, cmac(m11, b, zero));
     }
 }
 // Hadamard butterfly without its 1/sqrt2 (applied once per pass): (a, b) <- (a + b, a - b)
-template <int RBIT>
-__device__ __forceinline__ void hbfly(double2 (&v)[NR]) {
+template <int RBIT, typename V>
+__device__ __forceinline__ void hbfly(V (&v)[NR]) {
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
         if (j & (1 << RBIT)) continue;
-        const double2 a = v[j], b = v[j | (1 << RBIT)];
-        v[j] = make_double2(a.x + b.x, a.y + b.y);
-        v[j | (1 << RBIT)] = make_double2(a.x - b.x, a.y - b.y);
+        const V a = v[j], b = v[j | (1 << RBIT)];
+        v[j] = VT<V>::mk(a.x + b.x, a.y + b.y);
+        v[j | (1 << RBIT)] = VT<V>::mk(a.x - b.x, a.y - b.y);
     }
 }
 // In a lane-skewed or flipped slot (register slot 0 holds the |1> amplitude) the lane applies
 // X H X: (slot0, slot1) <- (slot1 - slot0, slot1 + slot0)
-template <int RBIT>
-__device__ __forceinline__ void hbfly_sk(double2 (&v)[NR], int skew) {
+template <int RBIT, typename V>
+__device__ __forceinline__ void hbfly_sk(V (&v)[NR], int skew) {
     if ((skew >> RBIT) & 1) {
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
             if (j & (1 << RBIT)) continue;
-            const double2 a = v[j], b = v[j | (1 << RBIT)];  // a holds |1>, b holds |0>
-            v[j] = make_double2(b.x - a.x, b.y - a.y);         // new |1> = (|0> - |1>)
-            v[j | (1 << RBIT)] = make_double2(b.x + a.x, b.y + a.y);
+            const V a = v[j], b = v[j | (1 << RBIT)];  // a holds |1>, b holds |0>
+            v[j] = VT<V>::mk(b.x - a.x, b.y - a.y);   // new |1> = (|0> - |1>)
+            v[j | (1 << RBIT)] = VT<V>::mk(b.x + a.x, b.y + a.y);
         }
     } else {
         hbfly<RBIT>(v);
     }
 }
-template <int F>
-__device__ __forceinline__ void hmix_frame(double2 (&v)[NR], unsigned mask, int skew = 0) {
+template <int F, typename V>
+__device__ __forceinline__ void hmix_frame(V (&v)[NR], unsigned mask, int skew = 0) {
     const unsigned m5 = (mask >> Frame<F>::RB) & 0x1Fu;
     if (m5 & 1) hbfly_sk<0>(v, skew);
     if (m5 & 2) hbfly_sk<1>(v, skew);
@@ -197,44 +228,51 @@ __device__ __forceinline__ void hmix_frame(double2 (&v)[NR], unsigned mask, int 
 
 // `skew`: register bits whose tile bit is inverted in this lane (the lane-skewed frame Y of the
 // TMA kernel); there register slot 0 holds the |1> amplitude, so the lane applies X M X
-template <int RBIT>
-__device__ __forceinline__ void gbfly_sk(double2 (&v)[NR], const double2 (&M)[4], int skew) {
+template <int RBIT, typename V>
+__device__ __forceinline__ void gbfly_sk(V (&v)[NR], const double2 (&M)[4], int skew) {
     const bool sw = (skew >> RBIT) & 1;
     const double2 G[4] = {sw ? M[3] : M[0], sw ? M[2] : M[1], sw ? M[1] : M[2], sw ? M[0] : M[3]};
     gbfly<RBIT>(v, G);
 }
-template <int F>
-__device__ __forceinline__ void gmix_frame(double2 (&v)[NR], unsigned mask, const double2 (&G)[KT][4],
+// skews reach register bits 0..2 (FP64 frame Y) or 0..3 (FP32 frames Y, W)
+template <int F, typename V>
+__device__ __forceinline__ void gmix_frame(V (&v)[NR], unsigned mask, const double2 (&G)[KT][4],
                                            int skew = 0) {
     const unsigned m5 = (mask >> Frame<F>::RB) & 0x1Fu;
     if (m5 & 1) gbfly_sk<0>(v, G[Frame<F>::RB + 0], skew);
     if (m5 & 2) gbfly_sk<1>(v, G[Frame<F>::RB + 1], skew);
     if (m5 & 4) gbfly_sk<2>(v, G[Frame<F>::RB + 2], skew);
-    if (m5 & 8) gbfly<3>(v, G[Frame<F>::RB + 3]);
+    if (m5 & 8) {
+        if (sizeof(V) == 8) gbfly_sk<3>(v, G[Frame<F>::RB + 3], skew);
+        else gbfly<3>(v, G[Frame<F>::RB + 3]);
+    }
     if (m5 & 16) gbfly<4>(v, G[Frame<F>::RB + 4]);
 }
 
 // runtime-frame variants (one copy of code for every frame): element t = tthr | ((j ^ sk) << rb)
-__device__ __forceinline__ void mix5(double2 (&v)[NR], unsigned m5, double t) {
+template <typename V>
+__device__ __forceinline__ void mix5(V (&v)[NR], unsigned m5, double t) {
     if (m5 & 1) bfly<0>(v, t);
     if (m5 & 2) bfly<1>(v, t);
     if (m5 & 4) bfly<2>(v, t);
     if (m5 & 8) bfly<3>(v, t);
     if (m5 & 16) bfly<4>(v, t);
 }
-__device__ __forceinline__ void lds_rt(double2 (&v)[NR], const double2 *sm, int tthr, int rb) {
+template <typename V>
+__device__ __forceinline__ void lds_rt(V (&v)[NR], const V *sm, int tthr, int rb, int sk = 0) {
 #pragma unroll
-    for (int j = 0; j < NR; ++j) v[j] = sm[tthr | (j << rb)];
+    for (int j = 0; j < NR; ++j) v[j] = sm[tthr | ((j ^ sk) << rb)];
 }
-__device__ __forceinline__ void sts_rt(const double2 (&v)[NR], double2 *sm, int tthr, int rb) {
+template <typename V>
+__device__ __forceinline__ void sts_rt(const V (&v)[NR], V *sm, int tthr, int rb, int sk = 0) {
 #pragma unroll
-    for (int j = 0; j < NR; ++j) sm[tthr | (j << rb)] = v[j];
+    for (int j = 0; j < NR; ++j) sm[tthr | ((j ^ sk) << rb)] = v[j];
 }
 
 // frame change through shared memory (one barrier); every thread writes back exactly
 // the elements it read in the previous exchange, so one barrier per exchange suffices.
-template <int F1, int F2>
-__device__ __forceinline__ void xch(double2 (&v)[NR], double2 *sm, int lane, int warp) {
+template <int F1, int F2, typename V>
+__device__ __forceinline__ void xch(V (&v)[NR], V *sm, int lane, int warp) {
     const int t1 = Frame<F1>::tthr(lane, warp);
 #pragma unroll
     for (int j = 0; j < NR; ++j) sm[swz(t1 | (j << Frame<F1>::RB))] = v[j];
@@ -255,8 +293,8 @@ __device__ __forceinline__ u64 thread_offset(const int *L, int lane, int warp) {
     return off;
 }
 
-template <int F>
-__device__ __forceinline__ void load_tile(double2 (&v)[NR], const double2 *base, const int *L) {
+template <int F, typename V>
+__device__ __forceinline__ void load_tile(V (&v)[NR], const V *base, const int *L) {
     const u64 s0 = 1ull << L[Frame<F>::RB], s1 = 1ull << L[Frame<F>::RB + 1], s2 = 1ull << L[Frame<F>::RB + 2],
               s3 = 1ull << L[Frame<F>::RB + 3], s4 = 1ull << L[Frame<F>::RB + 4];
 #pragma unroll
@@ -267,14 +305,16 @@ __device__ __forceinline__ void load_tile(double2 (&v)[NR], const double2 *base,
     }
 }
 
-template <int F>
-__device__ __forceinline__ void store_tile(const double2 (&v)[NR], double2 *base, const int *L) {
+// `sk`: the frame's lane skew (slot j holds register pattern j ^ sk, see frame_skew)
+template <int F, typename V>
+__device__ __forceinline__ void store_tile(const V (&v)[NR], V *base, const int *L, int sk = 0) {
     const u64 s0 = 1ull << L[Frame<F>::RB], s1 = 1ull << L[Frame<F>::RB + 1], s2 = 1ull << L[Frame<F>::RB + 2],
               s3 = 1ull << L[Frame<F>::RB + 3], s4 = 1ull << L[Frame<F>::RB + 4];
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-        const u64 o = ((j & 1) ? s0 : 0) + ((j & 2) ? s1 : 0) + ((j & 4) ? s2 : 0) + ((j & 8) ? s3 : 0) +
-                      ((j & 16) ? s4 : 0);
+        const int k = j ^ sk;
+        const u64 o = ((k & 1) ? s0 : 0) + ((k & 2) ? s1 : 0) + ((k & 4) ? s2 : 0) + ((k & 8) ? s3 : 0) +
+                      ((k & 16) ? s4 : 0);
         __stcs(base + o, v[j]);
     }
 }
@@ -340,6 +380,7 @@ __device__ inline double err_of(const double *Jp, int n, const int *L, int j) {
 // per-CTA launch constants and reduction scratch in shared memory
 struct CtaShared {
     double2 PRR[NR];     // e^{-i gamma E_RR(j)}
+    float2 PRRf[NR];     // the same in FP32 (FP32 precision mode)
     double eRR[NR];      // E_RR(j)
     double red[2][NTHR / 32];
 };
@@ -356,10 +397,14 @@ struct __align__(16) TileRec {
 //   E = E_H + sum_{i in T} s_i h'_i + E_TT + sum_r s_r (h'_{R_r} + w_r) + E_RR(j)
 // pconst = kappa-scale * e^{-i gamma E_TT};  u[r] = e^{-i gamma w_r}.
 // The register-bit factor is lo[j & 3] * hi[j >> 2] (conjugate symmetry halves the work).
-// tthr is the thread's tile index xor the tile-bit flips; fr = register-bit flips.
+// tthr is the thread's tile index xor the tile-bit flips; fr = register-bit flips; sk = the
+// frame's lane skew (register slot j holds register pattern j ^ sk; PRR is indexed by pattern).
+// FP32 states take the factor products in FP32 from FP64 tables (PRRf = PRR in FP32).
 template <int F>
 __device__ __forceinline__ void apply_phase(double2 (&v)[NR], const TileRec *R, int tthr, int fr, double2 pconst,
-                                            const double2 (&u)[5], const double2 *PRR) {
+                                            const double2 (&u)[5], const double2 *PRR, const float2 * = nullptr,
+                                            int sk = 0) {
+    fr ^= sk;  // slot j holds pattern j ^ sk: its spins are those of (j ^ sk ^ flips)
     double2 base = cmul(R->f[12], pconst);
 #pragma unroll
     for (int i = 0; i < KT; ++i) {
@@ -393,14 +438,53 @@ __device__ __forceinline__ void apply_phase(double2 (&v)[NR], const TileRec *R, 
     hi[2] = conjd(hi[5]);
     hi[3] = conjd(hi[4]);
 #pragma unroll
-    for (int j = 0; j < NR; ++j) v[j] = cmul(v[j], cmul(cmul(lo[j & 3], hi[j >> 2]), PRR[j]));
+    for (int j = 0; j < NR; ++j) v[j] = cmul(v[j], cmul(cmul(lo[j & 3], hi[j >> 2]), PRR[j ^ sk]));
+}
+template <int F>
+__device__ __forceinline__ void apply_phase(float2 (&v)[NR], const TileRec *R, int tthr, int fr, double2 pconst,
+                                            const double2 (&u)[5], const double2 *, const float2 *PRRf,
+                                            int sk = 0) {
+    fr ^= sk;  // slot j holds pattern j ^ sk: its spins are those of (j ^ sk ^ flips)
+    double2 base = cmul(R->f[12], pconst);
+#pragma unroll
+    for (int i = 0; i < KT; ++i) {
+        if (i >= Frame<F>::RB && i < Frame<F>::RB + 5) continue;
+        const double2 fi = R->f[i];
+        const double sg = ((tthr >> i) & 1) ? 1.0 : -1.0;
+        base = cmul(base, make_double2(fi.x, sg * fi.y));
+    }
+    double2 g[5];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+        const double2 gr = cmul(R->f[Frame<F>::RB + r], u[r]);
+        g[r] = ((fr >> r) & 1) ? conjd(gr) : gr;
+    }
+    const double2 A = cmul(g[0], g[1]), B = cmul(g[0], conjd(g[1]));
+    float2 lo[4];
+    lo[0] = vcast<float2>(cmul(base, conjd(A)));
+    lo[1] = vcast<float2>(cmul(base, B));
+    lo[2] = vcast<float2>(cmul(base, conjd(B)));
+    lo[3] = vcast<float2>(cmul(base, A));
+    const double2 C = cmul(g[2], g[3]), D = cmul(g[2], conjd(g[3]));
+    float2 hi[8];
+    hi[4] = vcast<float2>(cmul(conjd(C), g[4]));
+    hi[5] = vcast<float2>(cmul(D, g[4]));
+    hi[6] = vcast<float2>(cmul(conjd(D), g[4]));
+    hi[7] = vcast<float2>(cmul(C, g[4]));
+    hi[0] = make_float2(hi[7].x, -hi[7].y);
+    hi[1] = make_float2(hi[6].x, -hi[6].y);
+    hi[2] = make_float2(hi[5].x, -hi[5].y);
+    hi[3] = make_float2(hi[4].x, -hi[4].y);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) v[j] = cmul(v[j], cmul(cmul(lo[j & 3], hi[j >> 2]), PRRf[j ^ sk]));
 }
 
 // accumulate sum |psi|^2 E and sum |psi|^2 over the thread's 32 amplitudes (frame F)
-template <int F>
-__device__ __forceinline__ void accumulate(const double2 (&v)[NR], const TileRec *R, int tthr, int fr,
+template <int F, typename V>
+__device__ __forceinline__ void accumulate(const V (&v)[NR], const TileRec *R, int tthr, int fr,
                                            const ThreadEnergy &te, const double *eRR, double &acc_e,
-                                           double &acc_n) {
+                                           double &acc_n, int sk = 0) {
+    fr ^= sk;
     double Q[NR];
     double eb = R->e[12] + te.eTT;
 #pragma unroll
@@ -422,8 +506,9 @@ __device__ __forceinline__ void accumulate(const double2 (&v)[NR], const TileRec
     }
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-        const double p = fma(v[j].x, v[j].x, v[j].y * v[j].y);
-        acc_e = fma(p, Q[j] + eRR[j], acc_e);
+        const double2 a = dcast(v[j]);
+        const double p = fma(a.x, a.x, a.y * a.y);
+        acc_e = fma(p, Q[j] + eRR[j ^ sk], acc_e);
         acc_n += p;
     }
 }

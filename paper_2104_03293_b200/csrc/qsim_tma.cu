@@ -114,35 +114,47 @@ __device__ __forceinline__ void group_bar(int g) {
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// linear-layout frame I/O; frame Y skews its low register bits by the lane so that every
-// quarter-warp hits 8 different 16-byte bank groups
-template <int F>
-__device__ __forceinline__ void lds_frame(double2 (&v)[NR], const double2 *sm, int lane, int warp) {
+// linear-layout frame I/O; skewed frames (frame_skew) permute a lane's register slots so
+// that every wavefront hits distinct banks
+template <int F, typename V>
+__device__ __forceinline__ void lds_frame(V (&v)[NR], const V *sm, int lane, int warp) {
     const int t = Frame<F>::tthr(lane, warp);
-    const int sk = (F == FY) ? (lane & 7) : 0;
+    const int sk = frame_skew<F, V>(lane);
 #pragma unroll
     for (int j = 0; j < NR; ++j) v[j] = sm[t | ((j ^ sk) << Frame<F>::RB)];
 }
-template <int F>
-__device__ __forceinline__ void sts_frame(const double2 (&v)[NR], double2 *sm, int lane, int warp) {
+template <int F, typename V>
+__device__ __forceinline__ void sts_frame(const V (&v)[NR], V *sm, int lane, int warp) {
     const int t = Frame<F>::tthr(lane, warp);
-    const int sk = (F == FY) ? (lane & 7) : 0;
+    const int sk = frame_skew<F, V>(lane);
 #pragma unroll
     for (int j = 0; j < NR; ++j) sm[t | ((j ^ sk) << Frame<F>::RB)] = v[j];
 }
 
 struct TmaIssue {
     const CUtensorMap *tm;
+    const CUtensorMap *tms;  // output tensor map (TMA stores)
     const TileRec *grec;
-    double2 *stages;
+    unsigned char *stages;  // stage s at stages + s * SM_TILE_BYTES (FP32 tiles use half of it)
+    uint32_t tile_bytes;    // TILE * sizeof(amplitude)
     TileRec *srec;
     uint64_t *full;
     volatile int *issued;  // tiles issued into each stage so far
 };
 
-__device__ __forceinline__ void issue_tile(const PassParams &P, const TmaIssue &I, u64 ut, int s, bool load_state,
+// tile id of the CTA's k-th tile (PassParams::ord_rot; multi-GPU moving passes only)
+template <bool MV>
+__device__ __forceinline__ u64 tile_of(const PassParams &P, u64 k) {
+    if (!MV || !P.ord_rot) return k;
+    const u64 mask = (1ull << P.ord_bits) - 1ull;
+    return ((k << P.ord_rot) | (k >> (P.ord_bits - P.ord_rot))) & mask;
+}
+
+template <bool MV>
+__device__ __forceinline__ void issue_tile(const PassParams &P, const TmaIssue &I, u64 k, int s, bool load_state,
                                            bool load_rec) {
-    const uint32_t bytes = (load_state ? (uint32_t)SM_TILE_BYTES : 0u) + (load_rec ? (uint32_t)TILE_REC_BYTES : 0u);
+    const u64 ut = tile_of<MV>(P, k);
+    const uint32_t bytes = (load_state ? I.tile_bytes : 0u) + (load_rec ? (uint32_t)TILE_REC_BYTES : 0u);
     if (!bytes) {
         I.issued[s] = I.issued[s] + 1;
         return;
@@ -153,7 +165,7 @@ __device__ __forceinline__ void issue_tile(const PassParams &P, const TmaIssue &
 #pragma unroll
         for (int d = 0; d < 5; ++d)
             c[d] = P.tm_clen[d] ? (int)((ut >> P.tm_cshift[d]) & ((1ull << P.tm_clen[d]) - 1ull)) : 0;
-        tma_load_5d(I.stages + (size_t)s * TILE, I.tm, c, &I.full[s], P.l2hint & 3);
+        tma_load_5d(I.stages + (size_t)s * SM_TILE_BYTES, I.tm, c, &I.full[s], P.l2hint & 3);
     }
     if (load_rec) bulk_load(I.srec + s, I.grec + ut, (uint32_t)TILE_REC_BYTES, &I.full[s]);
     __threadfence_block();
@@ -175,31 +187,37 @@ constexpr unsigned TMX = 0xF80u, TMY = 0x01Fu, TMZ = 0x060u, TMW = 0x078u;
 
 // tile-major out-of-place store: the tile is written as one contiguous 64 KiB block (element
 // t at t), so every warp store covers >= 128 contiguous bytes and every CTA writes whole blocks
-template <int F>
-__device__ __forceinline__ void store_tile_major(const double2 (&v)[NR], const PassParams &P, u64 ut, int lane,
+template <int F, typename V>
+__device__ __forceinline__ void store_tile_major(const V (&v)[NR], const PassParams &P, u64 ut, int lane,
                                                  int warp) {
     u64 ou = 0;
     for (int k = 0; k < P.onseg; ++k) ou |= ((ut >> P.oseg_src[k]) & ((1ull << P.oseg_len[k]) - 1ull)) << P.oseg_dst[k];
-    double2 *base = P.out + (ou << KT) + Frame<F>::tthr(lane, warp);
+    V *base = reinterpret_cast<V *>(P.out) + (ou << KT) + Frame<F>::tthr(lane, warp);
 #pragma unroll
     for (int j = 0; j < NR; ++j) __stcs(base + (j << Frame<F>::RB), v[j]);
 }
 
 // store with the fused global-qubit swap: local index x = (c | y) with c the top
 // g local bits goes to rank c's other buffer at (rank | y); 1/G of the stores stay local, the
-// rest cross NVLink as 16-byte stores coalesced into >= 128-byte rows.
-template <int F>
-__device__ __forceinline__ void store_tile_swapped(const double2 (&v)[NR], const PassParams &P, u64 xb) {
+// rest cross NVLink as 16-byte stores coalesced into >= 128-byte rows.  With the split swap
+// only the amplitudes whose group (PassParams::mv_*) this pass owns move; the others are
+// written unswapped into the local other buffer (a later pass of the layer moves them).
+template <int F, typename V>
+__device__ __forceinline__ void store_tile_swapped(const V (&v)[NR], const PassParams &P, u64 xb) {
     const int sh = P.m - P.gbits;
     const u64 ymask = (1ull << sh) - 1ull;
     const u64 rofs = (u64)P.rank << sh;
+    const u64 pmask = (1ull << P.mv_pbits) - 1ull;
+    V *const own = reinterpret_cast<V *>(P.dst[P.rank]);
     const u64 s0 = 1ull << P.L[Frame<F>::RB], s1 = 1ull << P.L[Frame<F>::RB + 1], s2 = 1ull << P.L[Frame<F>::RB + 2],
               s3 = 1ull << P.L[Frame<F>::RB + 3], s4 = 1ull << P.L[Frame<F>::RB + 4];
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
         const u64 x = xb + ((j & 1) ? s0 : 0) + ((j & 2) ? s1 : 0) + ((j & 4) ? s2 : 0) + ((j & 8) ? s3 : 0) +
                       ((j & 16) ? s4 : 0);
-        __stcs(P.dst[x >> sh] + (rofs | (x & ymask)), v[j]);
+        const unsigned pr = (unsigned)((x >> P.mv_pshift) & pmask);
+        V *a = (pr >= P.mv_lo && pr < P.mv_hi) ? reinterpret_cast<V *>(P.dst[x >> sh]) + (rofs | (x & ymask)) : own + x;
+        __stcs(a, v[j]);
     }
 }
 
@@ -207,16 +225,19 @@ __device__ __forceinline__ void store_tile_swapped(const double2 (&v)[NR], const
 // mixer modes: GMIX 0 = scaled R_x, 1 = general per-bit 2x2, 2 = Hadamard
 #define MIXF(FR, MASK, WHICH)                                                             \
     do {                                                                                  \
-        if (GMIX == 1) gmix_frame<FR>(v, (MASK), (WHICH) == 1 ? P.gm1 : P.gm2, FR == FY ? (lane & 7) : 0); \
-        else if (GMIX == 2) hmix_frame<FR>(v, (MASK), (FR == FY ? (lane & 7) : 0) ^ ((ft >> Frame<FR>::RB) & 31)); \
+        if (GMIX == 1) gmix_frame<FR>(v, (MASK), (WHICH) == 1 ? P.gm1 : P.gm2, frame_skew<FR, V>(lane)); \
+        else if (GMIX == 2) hmix_frame<FR>(v, (MASK), frame_skew<FR, V>(lane) ^ ((ft >> Frame<FR>::RB) & 31)); \
         else mix_frame<FR>(v, (MASK), (WHICH) == 1 ? P.c1.t : P.c2.t);                     \
     } while (0)
 
-template <int KIND, int GMIX>
+// MV: multi-GPU variant (fused / split global-qubit swap stores, tile order rotation); the
+// single-GPU instances compile without that code (it costs ~3 % in the hot loop)
+template <int KIND, int GMIX, typename V, bool MV>
 __global__ void __launch_bounds__(TMA_NG * 128, 1)
-    tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassParams P) {
+    tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap smap,
+                    const PassParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
-    double2 *stages = reinterpret_cast<double2 *>(smem);
+    unsigned char *stages = smem;
     TileRec *srec = reinterpret_cast<TileRec *>(smem + TmaSmem::rec_off);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + TmaSmem::bar_off);
     CtaShared &cs = *reinterpret_cast<CtaShared *>(smem + TmaSmem::cs_off);
@@ -231,7 +252,10 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     const bool load_state = !(TURN && P.init) && !(P.dbg & 2);
     const u64 ntl = (P.ntiles > blockIdx.x) ? (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     volatile int *issued = reinterpret_cast<volatile int *>(smem + TmaSmem::iss_off);
-    const TmaIssue I{&tmap, reinterpret_cast<const TileRec *>(P.rec), stages, srec, full, issued};
+    const TmaIssue I{&tmap, MV ? &smap : &tmap, reinterpret_cast<const TileRec *>(P.rec), stages, (uint32_t)(TILE * sizeof(V)),
+                     srec, full, issued};
+// STG output base (out of place when moving), re-read from the parameter bank at each use
+#define OUTB (reinterpret_cast<V *>(MV && P.mv ? P.dst[P.rank] : P.psi))
 
     if (tid == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
@@ -243,7 +267,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     __syncthreads();
     if (tid == 0)
         for (int i = 0; i < NSTAGE && (u64)i < ntl; ++i)
-            issue_tile(P, I, blockIdx.x + (u64)i * gridDim.x, i, load_state, need_e);
+            issue_tile<MV>(P, I, blockIdx.x + (u64)i * gridDim.x, i, load_state, need_e);
 
     int ft = 0;  // tile-bit flips (X gates of the |tan beta| > 1 mixer form)
 #pragma unroll
@@ -271,19 +295,21 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             const double e = err_of<FE>(P.Jp, n, P.L, tid ^ fr);
             cs.eRR[tid] = e;
             cs.PRR[tid] = TURN ? expmi(P.gamma * e) : make_double2(1.0, 0.0);
+            cs.PRRf[tid] = vcast<float2>(cs.PRR[tid]);
         }
     }
     const u64 offX = thread_offset<FX>(P.L, lane, warp);
     const u64 offS = thread_offset<RUN ? FW : FZ>(P.L, lane, warp);
     __syncthreads();
 
+    const int skE = frame_skew<FE, V>(lane);  // skew of the phase / reduction frame
     double acc_e = 0.0, acc_n = 0.0;
-    double2 v[NR];
+    V v[NR];
     for (u64 i = g; i < ntl; i += TMA_NG) {
         const int s = (int)(i % NSTAGE);
-        const u64 ut = blockIdx.x + i * gridDim.x;
+        const u64 ut = tile_of<MV>(P, blockIdx.x + i * gridDim.x);
         const u64 tb = tile_base(P, ut);
-        double2 *sm = stages + (size_t)s * TILE;
+        V *sm = reinterpret_cast<V *>(stages + (size_t)s * SM_TILE_BYTES);
         const TileRec *R = srec + s;
         if (load_state || need_e) wait_tile(I, i);
         // ------------------------------------------------ compact turning-run body
@@ -291,11 +317,12 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         // phase, driven by four mix steps X(mix1) W(mix1) [phase] W(mix2) X(mix2))
         if constexpr (KIND == K_TURN_RUN && GMIX == 0) {
             const int tXt = Frame<FX>::tthr(lane, warp), tWt = Frame<FW>::tthr(lane, warp);
+            const int skW = frame_skew<FW, V>(lane);
             const unsigned mx1 = (P.mix1 & TMX) >> 7, mw1 = (P.mix1 & TMW) >> 3;
             const unsigned mw2 = (P.mix2 & TMW) >> 3, mx2 = (P.mix2 & TMX) >> 7;
             if (!load_state) {
 #pragma unroll
-                for (int j = 0; j < NR; ++j) v[j] = make_double2(P.a0, 0.0);
+                for (int j = 0; j < NR; ++j) v[j] = VT<V>::mk((typename VT<V>::S)P.a0, 0);
             }
             int prev = -1;  // frame of the registers: 0 = X, 1 = W
 #pragma unroll 1
@@ -303,28 +330,28 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 const int fr_now = (stp == 1 || stp == 2) ? 1 : 0;
                 if (load_state && fr_now != prev) {
                     if (prev >= 0) {
-                        sts_rt(v, sm, prev ? tWt : tXt, prev ? Frame<FW>::RB : Frame<FX>::RB);
+                        sts_rt(v, sm, prev ? tWt : tXt, prev ? Frame<FW>::RB : Frame<FX>::RB, prev ? skW : 0);
                         group_bar(g);
                     }
-                    lds_rt(v, sm, fr_now ? tWt : tXt, fr_now ? Frame<FW>::RB : Frame<FX>::RB);
+                    lds_rt(v, sm, fr_now ? tWt : tXt, fr_now ? Frame<FW>::RB : Frame<FX>::RB, fr_now ? skW : 0);
                 } else if (!load_state && stp == 3) {
-                    sts_rt(v, sm, tWt, Frame<FW>::RB);
+                    sts_rt(v, sm, tWt, Frame<FW>::RB, skW);
                     group_bar(g);
                     lds_rt(v, sm, tXt, Frame<FX>::RB);
                 }
                 prev = fr_now;
-                if (stp == 2) apply_phase<FW>(v, R, tE, fr, pconst, u, cs.PRR);
+                if (stp == 2) apply_phase<FW>(v, R, tE, fr, pconst, u, cs.PRR, cs.PRRf, skW);
                 if (stp == 3) {  // last smem read done: release the stage unless TMA-storing
-                    if (!(P.tma_store && !P.swap_store && !P.tmo)) {
+                    if (!(P.tma_store && !(MV && P.swap_store) && !P.tmo)) {
                         fence_async_smem();
                         group_bar(g);
                         if (gt == 0 && i + NSTAGE < ntl)
-                            issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                            issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
                     }
                 }
                 mix5(v, stp == 0 ? mx1 : stp == 1 ? mw1 : stp == 2 ? mw2 : mx2, stp < 2 ? P.c1.t : P.c2.t);
             }
-            if (P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
+            if (MV && P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
             else if (P.tmo) store_tile_major<FX>(v, P, ut, lane, warp);
             else if (P.tma_store) {
                 sts_rt(v, sm, tXt, Frame<FX>::RB);
@@ -333,12 +360,12 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 if (gt == 0) {
                     int c[5];
                     tile_coords(P, ut, c);
-                    tma_store_5d(I.tm, c, sm, (P.l2hint >> 2) & 3);
+                    tma_store_5d(I.tms, c, sm, (P.l2hint >> 2) & 3);
                     bulk_wait_read0();
-                    if (i + NSTAGE < ntl) issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                    if (i + NSTAGE < ntl) issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
                 }
             } else
-                store_tile<FX>(v, P.psi + tb + offX, P.L);
+                store_tile<FX>(v, OUTB + tb + offX, P.L);
         } else {
         // ------------------------------------------------ rounds up to the last smem read
         if (load_state) {
@@ -359,14 +386,15 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < NR; ++j) v[j] = make_double2(P.a0, 0.0);
+            for (int j = 0; j < NR; ++j) v[j] = VT<V>::mk((typename VT<V>::S)P.a0, 0);
         }
         if (TURN) {
             if (GMIX == 2) {  // no phase; the pass-wide 2^{-m/2} of the Hadamards
+                const typename VT<V>::S sc = (typename VT<V>::S)P.scale.x;
 #pragma unroll
-                for (int j = 0; j < NR; ++j) v[j] = make_double2(v[j].x * P.scale.x, v[j].y * P.scale.x);
+                for (int j = 0; j < NR; ++j) v[j] = VT<V>::mk(v[j].x * sc, v[j].y * sc);
             } else if (!(GMIX == 1 && P.gamma == 0.0 && P.scale.x == 1.0 && P.scale.y == 0.0))  // identity phase
-                apply_phase<FE>(v, R, tE, fr, pconst, u, cs.PRR);
+                apply_phase<FE>(v, R, tE, fr, pconst, u, cs.PRR, cs.PRRf, skE);
             if (RUN) {
                 MIXF(FW, P.mix2 & TMW, 2);
                 sts_frame<FW>(v, sm, lane, warp);
@@ -385,18 +413,18 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         // ------------------------------------------------ release the stage, refill it
         // (a reducing pass reads the stage's tile record, so it finishes before the refill)
         // TMA-store mode keeps the stage until the store has read it back
-        const bool tstore = P.tma_store && !P.swap_store && !P.tmo && !(P.dbg & 1);
+        const bool tstore = P.tma_store && !(MV && P.swap_store) && !P.tmo && !(P.dbg & 1);
         const bool late_release = (!TURN && P.reduce) || tstore;
         if (!late_release) {
             fence_async_smem();
             group_bar(g);
             if (gt == 0 && i + NSTAGE < ntl)
-                issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
         }
         // ------------------------------------------------ finish in registers, store
         if (TURN) {
             MIXF(FX, P.mix2 & TMX, 2);
-            if (P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
+            if (MV && P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
             else if (P.tmo) store_tile_major<FX>(v, P, ut, lane, warp);
             else if (tstore) {
                 sts_frame<FX>(v, sm, lane, warp);
@@ -405,12 +433,12 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 if (gt == 0) {
                     int c[5];
                     tile_coords(P, ut, c);
-                    tma_store_5d(I.tm, c, sm, (P.l2hint >> 2) & 3);
+                    tma_store_5d(I.tms, c, sm, (P.l2hint >> 2) & 3);
                     bulk_wait_read0();
-                    if (i + NSTAGE < ntl) issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                    if (i + NSTAGE < ntl) issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
                 }
             } else
-                store_tile<FX>(v, P.psi + tb + offX, P.L);
+                store_tile<FX>(v, OUTB + tb + offX, P.L);
         } else {
             if (RUN) MIXF(FW, P.mix1 & TMW, 1);
             else MIXF(FZ, P.mix1 & TMZ, 1);
@@ -418,14 +446,32 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 double s = 0.0;
 #pragma unroll
                 for (int j = 0; j < NR; ++j) s += v[j].x;
-                if (s == 12345.678) P.psi[0] = v[0];
+                if (s == 12345.678) OUTB[0] = v[0];
                 continue;
             }
             if (P.scale.x != 1.0 || P.scale.y != 0.0) {
+                const V sc = vcast<V>(P.scale);
 #pragma unroll
-                for (int j = 0; j < NR; ++j) v[j] = cmul(v[j], P.scale);
+                for (int j = 0; j < NR; ++j) v[j] = cmul(v[j], sc);
             }
-            if (P.reduce) accumulate<FE>(v, R, tE, fr, te, cs.eRR, acc_e, acc_n);
+            if (P.reduce) accumulate<FE>(v, R, tE, fr, te, cs.eRR, acc_e, acc_n, skE);
+            if (MV && P.mv == 1) {  // split swap: this tile may belong to a peer (whole tile moves)
+                const int sh = P.m - P.gbits;
+                const unsigned vr = (unsigned)((tb >> sh) & ((1ull << P.gbits) - 1ull));
+                const unsigned pr = (unsigned)((tb >> P.mv_pshift) & ((1ull << P.mv_pbits) - 1ull));
+                if (vr != (unsigned)P.rank && pr >= P.mv_lo && pr < P.mv_hi) {
+                    if (late_release) {
+                        fence_async_smem();
+                        group_bar(g);
+                        if (gt == 0 && i + NSTAGE < ntl)
+                            issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                    }
+                    const u64 wm = ((1ull << P.gbits) - 1ull) << sh;
+                    store_tile<RUN ? FW : FZ>(v, reinterpret_cast<V *>(P.dst[vr]) + ((tb & ~wm) | ((u64)P.rank << sh)) + offS,
+                                              P.L, skE);
+                    continue;
+                }
+            }
             if (tstore) {
                 sts_frame<RUN ? FW : FZ>(v, sm, lane, warp);
                 fence_async_smem();
@@ -433,9 +479,9 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 if (gt == 0) {
                     int c[5];
                     tile_coords(P, ut, c);
-                    tma_store_5d(I.tm, c, sm, (P.l2hint >> 2) & 3);
+                    tma_store_5d(I.tms, c, sm, (P.l2hint >> 2) & 3);
                     bulk_wait_read0();
-                    if (i + NSTAGE < ntl) issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                    if (i + NSTAGE < ntl) issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
                 }
                 continue;
             }
@@ -443,14 +489,14 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 fence_async_smem();
                 group_bar(g);
                 if (gt == 0 && i + NSTAGE < ntl)
-                    issue_tile(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                    issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
             }
             if (P.tmo) store_tile_major<RUN ? FW : FZ>(v, P, ut, lane, warp);
-            else store_tile<RUN ? FW : FZ>(v, P.psi + tb + offS, P.L);
+            else store_tile<RUN ? FW : FZ>(v, OUTB + tb + offS, P.L, skE);
         }
         }  // generic body
     }
-    if (P.swap_store) __threadfence_system();  // NVLink stores visible before the pass completes
+    if (MV && (P.swap_store || P.mv)) __threadfence_system();  // NVLink stores visible before the pass completes
     if (P.reduce) {
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
@@ -477,46 +523,67 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
 
 size_t tma_smem_bytes() { return TmaSmem::total; }
 
-template <int GMIX>
+template <int GMIX, typename V, bool MV>
 cudaError_t setup_tma_kernels_g() {
+    const int sh = (int)TmaSmem::total;
     cudaError_t e;
-    e = cudaFuncSetAttribute(tma_pass_kernel<K_PLAIN12, GMIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
+    e = cudaFuncSetAttribute(tma_pass_kernel<K_PLAIN12, GMIX, V, MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(tma_pass_kernel<K_PLAIN_RUN, GMIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
+    e = cudaFuncSetAttribute(tma_pass_kernel<K_PLAIN_RUN, GMIX, V, MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(tma_pass_kernel<K_TURN12, GMIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
+    e = cudaFuncSetAttribute(tma_pass_kernel<K_TURN12, GMIX, V, MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(tma_pass_kernel<K_TURN_RUN, GMIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaSmem::total);
+    return cudaFuncSetAttribute(tma_pass_kernel<K_TURN_RUN, GMIX, V, MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
+}
+
+template <typename V, bool MV>
+cudaError_t setup_tma_kernels_v() {
+    cudaError_t e = setup_tma_kernels_g<0, V, MV>();
+    if (e == cudaSuccess) e = setup_tma_kernels_g<1, V, MV>();
+    if (e == cudaSuccess) e = setup_tma_kernels_g<2, V, MV>();
+    return e;
 }
 
 cudaError_t setup_tma_kernels() {
-    cudaError_t e = setup_tma_kernels_g<0>();
-    if (e != cudaSuccess) return e;
-    e = setup_tma_kernels_g<1>();
-    if (e != cudaSuccess) return e;
-    return setup_tma_kernels_g<2>();
+    cudaError_t e = setup_tma_kernels_v<double2, false>();
+    if (e == cudaSuccess) e = setup_tma_kernels_v<double2, true>();
+    if (e == cudaSuccess) e = setup_tma_kernels_v<float2, false>();
+    if (e == cudaSuccess) e = setup_tma_kernels_v<float2, true>();
+    return e;
 }
 
-template <int GMIX>
-cudaError_t launch_tma_pass_g(const CUtensorMap &tm, const PassParams &P, int grid, cudaStream_t s) {
+template <int GMIX, typename V, bool MV>
+cudaError_t launch_tma_pass_g(const CUtensorMap &tm, const CUtensorMap &sm, const PassParams &P, int grid,
+                              cudaStream_t s) {
     const size_t sh = TmaSmem::total;
     switch (P.kind) {
-        case K_PLAIN12: tma_pass_kernel<K_PLAIN12, GMIX><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
-        case K_PLAIN_RUN: tma_pass_kernel<K_PLAIN_RUN, GMIX><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
-        case K_TURN12: tma_pass_kernel<K_TURN12, GMIX><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
-        case K_TURN_RUN: tma_pass_kernel<K_TURN_RUN, GMIX><<<grid, TMA_NG * 128, sh, s>>>(tm, P); break;
+        case K_PLAIN12: tma_pass_kernel<K_PLAIN12, GMIX, V, MV><<<grid, TMA_NG * 128, sh, s>>>(tm, sm, P); break;
+        case K_PLAIN_RUN: tma_pass_kernel<K_PLAIN_RUN, GMIX, V, MV><<<grid, TMA_NG * 128, sh, s>>>(tm, sm, P); break;
+        case K_TURN12: tma_pass_kernel<K_TURN12, GMIX, V, MV><<<grid, TMA_NG * 128, sh, s>>>(tm, sm, P); break;
+        case K_TURN_RUN: tma_pass_kernel<K_TURN_RUN, GMIX, V, MV><<<grid, TMA_NG * 128, sh, s>>>(tm, sm, P); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_tma_pass(const CUtensorMap &tm, const PassParams &P, int grid, cudaStream_t s) {
+template <typename V, bool MV>
+cudaError_t launch_tma_pass_v(const CUtensorMap &tm, const CUtensorMap &sm, const PassParams &P, int grid,
+                              cudaStream_t s) {
     switch (P.gmix) {
-        case 0: return launch_tma_pass_g<0>(tm, P, grid, s);
-        case 1: return launch_tma_pass_g<1>(tm, P, grid, s);
-        case 2: return launch_tma_pass_g<2>(tm, P, grid, s);
+        case 0: return launch_tma_pass_g<0, V, MV>(tm, sm, P, grid, s);
+        case 1: return launch_tma_pass_g<1, V, MV>(tm, sm, P, grid, s);
+        case 2: return launch_tma_pass_g<2, V, MV>(tm, sm, P, grid, s);
         default: return cudaErrorInvalidValue;
     }
+}
+
+// multi-GPU handles (P.multi) launch the MV instances for every pass
+cudaError_t launch_tma_pass(const CUtensorMap &tm, const CUtensorMap &sm, const PassParams &P, int grid,
+                            cudaStream_t s) {
+    if (P.f32) return P.multi ? launch_tma_pass_v<float2, true>(tm, sm, P, grid, s)
+                              : launch_tma_pass_v<float2, false>(tm, sm, P, grid, s);
+    return P.multi ? launch_tma_pass_v<double2, true>(tm, sm, P, grid, s)
+                   : launch_tma_pass_v<double2, false>(tm, sm, P, grid, s);
 }
 
 }  // namespace qk

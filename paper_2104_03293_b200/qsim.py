@@ -27,6 +27,7 @@ QSIM_ECUDA = -6
 QSIM_ENCCL = -7
 QSIM_FP64 = 0
 QSIM_FP32 = 1
+QSIM_FP32 = 1
 
 _ERRNAMES = {QSIM_EINVAL: "EINVAL", QSIM_ENOMEM: "ENOMEM", QSIM_ERANGE: "ERANGE",
              QSIM_ESTATE: "ESTATE", QSIM_EUNSUPPORTED: "EUNSUPPORTED", QSIM_ECUDA: "ECUDA",
@@ -38,7 +39,7 @@ EXPORTS = ["qsim_create", "qsim_create_ex", "qsim_destroy", "qsim_set_ising", "q
            "qsim_success_prob", "qsim_get_amplitudes", "qsim_energies", "qsim_spin_expectations",
            "qsim_apply_aqa_traced", "qsim_ground_states", "qsim_enumerate", "qsim_sync",
            "qsim_plan_counts", "qsim_plan_positions", "qsim_nccl_unique_id",
-           "qsim_bench_pass", "qsim_profile_enable", "qsim_profile_read", "qsim_kernel_launches", "qsim_last_error",
+           "qsim_bench_pass", "qsim_profile_enable", "qsim_profile_read", "qsim_profile_passes", "qsim_kernel_launches", "qsim_last_error",
            "qsim_version"]
 
 
@@ -85,6 +86,7 @@ lib.qsim_nccl_unique_id.argtypes = [ctypes.c_void_p]
 lib.qsim_bench_pass.argtypes = [_H, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D]
 lib.qsim_profile_enable.argtypes = [_H, ctypes.c_int]
 lib.qsim_profile_read.argtypes = [_H, _D, _U64, _D]
+lib.qsim_profile_passes.argtypes = [_H, _D, ctypes.c_int]
 lib.qsim_kernel_launches.argtypes = [_H]
 lib.qsim_kernel_launches.restype = ctypes.c_uint64
 lib.qsim_last_error.argtypes = [_H]
@@ -277,6 +279,14 @@ def qsim_profile_read(h):
     return ms.value, cnt.value, by.value
 
 
+def qsim_profile_passes(h, cap: int = 4096):
+    """-> per-pass durations (ms) of the recorded passes, in launch order"""
+    out = np.zeros(cap)
+    rc = lib.qsim_profile_passes(h, out.ctypes.data_as(_D), cap)
+    _check(min(rc, 0), h)
+    return out[: min(rc, cap)].copy()
+
+
 def qsim_kernel_launches(h) -> int:
     return int(lib.qsim_kernel_launches(h))
 
@@ -295,14 +305,16 @@ class QSim:
     per GPU): QSim(n, rank=r, world=G, nccl_unique_id=uid)."""
 
     def __init__(self, n: int, rank: int = 0, world: int = 1, nccl_unique_id: bytes | None = None,
-                 state_buf: int | None = None, buf_bytes: int = 0, cuda_stream: int | None = None):
+                 state_buf: int | None = None, buf_bytes: int = 0, cuda_stream: int | None = None,
+                 precision: int = QSIM_FP64):
         self.n = n
         self.rank = rank
         self.world = world
+        self.precision = precision
         if world == 1 and state_buf is None and cuda_stream is None:
-            self.h = qsim_create(n)
+            self.h = qsim_create(n, precision)
         else:
-            self.h = qsim_create_ex(n, QSIM_FP64, rank, world, nccl_unique_id, state_buf, buf_bytes,
+            self.h = qsim_create_ex(n, precision, rank, world, nccl_unique_id, state_buf, buf_bytes,
                                     cuda_stream)
 
     def close(self):

@@ -137,8 +137,8 @@ def test_create_without_gpu_fails_loudly(Q):
 
 def test_create_rejects_bad_arguments(Q):
     with pytest.raises(Q.QsimError) as ei:
-        Q.qsim_create(10, Q.QSIM_FP32)
-    assert ei.value.code == Q.QSIM_EUNSUPPORTED
+        Q.qsim_create(10, 7)  # neither QSIM_FP64 nor QSIM_FP32
+    assert ei.value.code == Q.QSIM_EINVAL
     with pytest.raises(Q.QsimError) as ei:
         Q.qsim_create(0)
     assert ei.value.code == Q.QSIM_EINVAL

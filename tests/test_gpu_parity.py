@@ -199,8 +199,8 @@ def test_two_sat_config1_grid(Q):
 # ------------------------------------------------------------------ errors
 def test_error_codes(Q):
     with pytest.raises(Q.QsimError) as ei:
-        Q.qsim_create(12, Q.QSIM_FP32)
-    assert ei.value.code == Q.QSIM_EUNSUPPORTED
+        Q.qsim_create(12, 7)  # unknown precision
+    assert ei.value.code == Q.QSIM_EINVAL
     with Q.QSim(14) as s:
         with pytest.raises(Q.QsimError) as ei:
             s.apply_qaoa([0.1], [0.2])

@@ -105,6 +105,22 @@ for n in a.qubits:
     if rank == 0 and n <= 24:
         ref = o.qsds_state(h, J, 0.35, 3, s_, A, B)
         report(f"n={n} QSDS amplitudes", np.max(np.abs(psi_q - ref)) <= 1e-10)
+    # 1d) FP32 precision mode (NEXT-4) on the sharded handle: the DESIGN §9 bound
+    sim = Q.QSim(n, rank=rank, world=world, nccl_unique_id=new_uid(), precision=Q.QSIM_FP32)
+    sim.set_ising(h, J)
+    sim.init_plus()
+    sim.apply_qaoa(g, b)
+    e32 = sim.expect_hc()
+    psi32 = sim.amplitudes() if n <= 24 else None
+    sim.close()
+    if rank == 0 and n <= 24:
+        ref = o.qaoa_state(h, J, g, b)
+        bound = len(g) * (2 * n + 12) * 2.0 ** -24
+        d = np.linalg.norm(psi32 - ref)
+        er, sc = o.expect_hc(h, J, ref, with_abs=True)
+        emax = np.max(np.abs(o.energies(h, J)))
+        report(f"n={n} FP32 amplitudes", d <= bound, f"l2={d:.2e} bound={bound:.2e}")
+        report(f"n={n} FP32 <H_C>", abs(e32 - er) <= 2 * bound * emax + 1e-9 * sc, f"{e32:.9f} vs {er:.9f}")
     # 1b) p = 1 closed-form <H_C> (pin P4), any n
     sim = Q.QSim(n, rank=rank, world=world, nccl_unique_id=new_uid())
     sim.set_ising(h, J)

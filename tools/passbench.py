@@ -11,6 +11,7 @@ import torch  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, nargs="+", default=[30])
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--f32", action="store_true", help="FP32 state (8 B per amplitude)")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 from paper_2104_03293_b200 import instances as inst  # noqa: E402
@@ -18,10 +19,10 @@ from paper_2104_03293_b200 import qsim as Q  # noqa: E402
 
 for n in a.n:
     h, J = inst.random_ising(n, 1)
-    with Q.QSim(n) as s:
+    with Q.QSim(n, precision=Q.QSIM_FP32 if a.f32 else Q.QSIM_FP64) as s:
         s.set_ising(h, J)
         nsets = 1 + -(-(n - 12) // 9) + (1 if n >= 21 else 0)  # + the tile-major shape
-        ideal = 32 * 2.0 ** n / 6455.9e9 * 1e3
+        ideal = (16 if a.f32 else 32) * 2.0 ** n / 6455.9e9 * 1e3
         for k in range(nsets):
             for ph in (-3, -2, -1, 0, 1):
                 try:
