@@ -131,11 +131,16 @@ TileSet make_set(int m, const std::vector<int> &Lpos, unsigned own, int es = 16)
 // mixed bits taken top-down from bit m-1, each completed to 12 tile bits with the
 // lowest bits as unmixed "passengers" (>= minpass of them: 3 -> >= 128-byte coalesced rows in
 // FP64, 64-byte rows in FP32 unless minpass = 4).
+// The runs are balanced (lengths differ by at most one): the pass count is fixed by the longest
+// allowed run, and shorter runs leave more passengers, i.e. longer contiguous rows.
 std::vector<TileSet> build_sets(int m, int es = 16, int minpass = 3) {
     std::vector<std::pair<int, int>> runs;  // [a, a+len)
+    const int maxrun = qk::KT - minpass;
+    const int K = m > qk::KT ? (m - qk::KT + maxrun - 1) / maxrun : 0;
     int end = m;
-    while (end > qk::KT) {
-        int len = std::min(qk::KT - minpass, end - qk::KT);
+    for (int k = 0; k < K; ++k) {
+        const int rem = end - qk::KT, left = K - k;
+        const int len = (rem + left - 1) / left;  // the top runs take the ceiling
         runs.push_back({end - len, len});
         end -= len;
     }

@@ -148,6 +148,9 @@ __device__ __forceinline__ int frame_skew(int lane) {
 // (t = -cot beta, kappa = -i sin beta): the X gates commute with every mixer and are
 // tracked as an index flip mask F (state holds psi_{x xor F} at physical index x), so
 // there is one butterfly form and no data movement for them.
+// (FP32: the packed FFMA2 form of these butterflies was measured slower on B200 -- FFMA2 runs at
+// half the instruction rate of FFMA, so it saves no FP32 pipe time, and its register pairing
+// added ~300 moves per turning pass; the scalar form is kept.)
 template <int RBIT, typename V>
 __device__ __forceinline__ void bfly(V (&v)[NR], double td) {
     typedef typename VT<V>::S S;
