@@ -164,15 +164,56 @@ __device__ __forceinline__ void bfly(V (&v)[NR], double td) {
     }
 }
 
+// Butterfly stages on the register bits of a 5-bit mask m5.  The masks that occur (a contiguous
+// block of register bits: all five, the part of a run in frame W or X, the arriving global
+// qubits, frame Z of the 12-bit set) run as straight-line code: a run-time test per stage makes
+// every stage a control-flow join, where the compiler must return the half of the outputs it
+// renamed to their home registers (64 moves per 64 DFMA, measured in the SASS; straight-line
+// stages have none).  `St` supplies the stage: St::template go<R>(v) mixes register bit R.
+template <unsigned M, class St, typename V>
+__device__ __forceinline__ void stages_c(V (&v)[NR], const St &st) {
+    if (M & 1u) st.template go<0>(v);
+    if (M & 2u) st.template go<1>(v);
+    if (M & 4u) st.template go<2>(v);
+    if (M & 8u) st.template go<3>(v);
+    if (M & 16u) st.template go<4>(v);
+}
+// FS: the frame (its straight-line mask set); -1 = the union (the runtime-frame turning body)
+template <int FS, class St, typename V>
+__device__ __forceinline__ void stages(V (&v)[NR], unsigned m5, const St &st) {
+    constexpr bool X = St::kFast && (FS == -1 || FS == FX), W = St::kFast && (FS == -1 || FS == FW);
+    if (m5 == 0u) return;
+    if (St::kFast && m5 == 0x1Fu && FS != FZ) stages_c<0x1Fu>(v, st);
+    else if (W && m5 == 0x0Fu) stages_c<0x0Fu>(v, st);
+    else if (W && m5 == 0x0Eu) stages_c<0x0Eu>(v, st);
+    else if (W && m5 == 0x0Cu) stages_c<0x0Cu>(v, st);
+    else if (W && m5 == 0x08u) stages_c<0x08u>(v, st);
+    else if (X && m5 == 0x10u) stages_c<0x10u>(v, st);
+    else if (X && m5 == 0x18u) stages_c<0x18u>(v, st);
+    else if (X && m5 == 0x1Cu) stages_c<0x1Cu>(v, st);
+    else if (St::kFast && FS == FZ && m5 == 0x03u) stages_c<0x03u>(v, st);
+    else {
+        if (m5 & 1) st.template go<0>(v);
+        if (m5 & 2) st.template go<1>(v);
+        if (m5 & 4) st.template go<2>(v);
+        if (m5 & 8) st.template go<3>(v);
+        if (m5 & 16) st.template go<4>(v);
+    }
+}
+struct RxStage {  // scaled R_x butterfly
+    static constexpr bool kFast = true;
+    double t;
+    template <int R, typename V> __device__ __forceinline__ void go(V (&v)[NR]) const { bfly<R>(v, t); }
+};
+template <typename V>
+__device__ __forceinline__ void mix5(V (&v)[NR], unsigned m5, double t) {
+    stages<-1>(v, m5, RxStage{t});
+}
+
 // mix the tile bits of `mask` that are register bits of frame F
 template <int F, typename V>
 __device__ __forceinline__ void mix_frame(V (&v)[NR], unsigned mask, double t) {
-    const unsigned m5 = (mask >> Frame<F>::RB) & 0x1Fu;
-    if (m5 & 1) bfly<0>(v, t);
-    if (m5 & 2) bfly<1>(v, t);
-    if (m5 & 4) bfly<2>(v, t);
-    if (m5 & 8) bfly<3>(v, t);
-    if (m5 & 16) bfly<4>(v, t);
+    stages<F>(v, (mask >> Frame<F>::RB) & 0x1Fu, RxStage{t});
 }
 
 // general 2x2 butterfly: (a, b) <- (m00 a + m01 b, m10 a + m11 b)
@@ -205,28 +246,27 @@ __device__ __forceinline__ void hbfly(V (&v)[NR]) {
 }
 // In a lane-skewed or flipped slot (register slot 0 holds the |1> amplitude) the lane applies
 // X H X: (slot0, slot1) <- (slot1 - slot0, slot1 + slot0)
+// Branch-free for both: with sg = -1 in such a slot (+1 otherwise), (a, b) <- (sg a + b, a - sg b).
 template <int RBIT, typename V>
 __device__ __forceinline__ void hbfly_sk(V (&v)[NR], int skew) {
-    if ((skew >> RBIT) & 1) {
+    typedef typename VT<V>::S S;
+    const S sg = ((skew >> RBIT) & 1) ? (S)-1 : (S)1;
 #pragma unroll
-        for (int j = 0; j < NR; ++j) {
-            if (j & (1 << RBIT)) continue;
-            const V a = v[j], b = v[j | (1 << RBIT)];  // a holds |1>, b holds |0>
-            v[j] = VT<V>::mk(b.x - a.x, b.y - a.y);   // new |1> = (|0> - |1>)
-            v[j | (1 << RBIT)] = VT<V>::mk(b.x + a.x, b.y + a.y);
-        }
-    } else {
-        hbfly<RBIT>(v);
+    for (int j = 0; j < NR; ++j) {
+        if (j & (1 << RBIT)) continue;
+        const V a = v[j], b = v[j | (1 << RBIT)];
+        v[j] = VT<V>::mk(fma(sg, a.x, b.x), fma(sg, a.y, b.y));
+        v[j | (1 << RBIT)] = VT<V>::mk(fma(-sg, b.x, a.x), fma(-sg, b.y, a.y));
     }
 }
+struct HStage {
+    static constexpr bool kFast = true;
+    int skew;
+    template <int R, typename V> __device__ __forceinline__ void go(V (&v)[NR]) const { hbfly_sk<R>(v, skew); }
+};
 template <int F, typename V>
 __device__ __forceinline__ void hmix_frame(V (&v)[NR], unsigned mask, int skew = 0) {
-    const unsigned m5 = (mask >> Frame<F>::RB) & 0x1Fu;
-    if (m5 & 1) hbfly_sk<0>(v, skew);
-    if (m5 & 2) hbfly_sk<1>(v, skew);
-    if (m5 & 4) hbfly_sk<2>(v, skew);
-    if (m5 & 8) hbfly_sk<3>(v, skew);
-    if (m5 & 16) hbfly_sk<4>(v, skew);
+    stages<F>(v, (mask >> Frame<F>::RB) & 0x1Fu, HStage{skew});
 }
 
 // `skew`: register bits whose tile bit is inverted in this lane (the lane-skewed frame Y of the
@@ -238,29 +278,25 @@ __device__ __forceinline__ void gbfly_sk(V (&v)[NR], const double2 (&M)[4], int 
     gbfly<RBIT>(v, G);
 }
 // skews reach register bits 0..2 (FP64 frame Y) or 0..3 (FP32 frames Y, W)
+template <int RB>
+struct GStage {
+    // general 2x2 stages are 4x the FMAs: straight-line copies of them would overflow the
+    // instruction cache, so they keep the per-stage tests (moves are 1/4 of their work)
+    static constexpr bool kFast = false;
+    const double2 (*G)[4];  // G[tile bit]
+    int skew;
+    template <int R, typename V> __device__ __forceinline__ void go(V (&v)[NR]) const {
+        if (R < 3 || (R == 3 && sizeof(V) == 8)) gbfly_sk<R>(v, G[RB + R], skew);
+        else gbfly<R>(v, G[RB + R]);
+    }
+};
 template <int F, typename V>
 __device__ __forceinline__ void gmix_frame(V (&v)[NR], unsigned mask, const double2 (&G)[KT][4],
                                            int skew = 0) {
-    const unsigned m5 = (mask >> Frame<F>::RB) & 0x1Fu;
-    if (m5 & 1) gbfly_sk<0>(v, G[Frame<F>::RB + 0], skew);
-    if (m5 & 2) gbfly_sk<1>(v, G[Frame<F>::RB + 1], skew);
-    if (m5 & 4) gbfly_sk<2>(v, G[Frame<F>::RB + 2], skew);
-    if (m5 & 8) {
-        if (sizeof(V) == 8) gbfly_sk<3>(v, G[Frame<F>::RB + 3], skew);
-        else gbfly<3>(v, G[Frame<F>::RB + 3]);
-    }
-    if (m5 & 16) gbfly<4>(v, G[Frame<F>::RB + 4]);
+    stages<F>(v, (mask >> Frame<F>::RB) & 0x1Fu, GStage<Frame<F>::RB>{G, skew});
 }
 
 // runtime-frame variants (one copy of code for every frame): element t = tthr | ((j ^ sk) << rb)
-template <typename V>
-__device__ __forceinline__ void mix5(V (&v)[NR], unsigned m5, double t) {
-    if (m5 & 1) bfly<0>(v, t);
-    if (m5 & 2) bfly<1>(v, t);
-    if (m5 & 4) bfly<2>(v, t);
-    if (m5 & 8) bfly<3>(v, t);
-    if (m5 & 16) bfly<4>(v, t);
-}
 template <typename V>
 __device__ __forceinline__ void lds_rt(V (&v)[NR], const V *sm, int tthr, int rb, int sk = 0) {
 #pragma unroll
