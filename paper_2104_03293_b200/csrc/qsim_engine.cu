@@ -133,14 +133,15 @@ TileSet make_set(int m, const std::vector<int> &Lpos, unsigned own, int es = 16)
 // FP64, 64-byte rows in FP32 unless minpass = 4).
 // The runs are balanced (lengths differ by at most one): the pass count is fixed by the longest
 // allowed run, and shorter runs leave more passengers, i.e. longer contiguous rows.
-std::vector<TileSet> build_sets(int m, int es = 16, int minpass = 3) {
+std::vector<TileSet> build_sets(int m, int es = 16, int minpass = 3, bool balanced = true) {
     std::vector<std::pair<int, int>> runs;  // [a, a+len)
     const int maxrun = qk::KT - minpass;
     const int K = m > qk::KT ? (m - qk::KT + maxrun - 1) / maxrun : 0;
     int end = m;
     for (int k = 0; k < K; ++k) {
         const int rem = end - qk::KT, left = K - k;
-        const int len = (rem + left - 1) / left;  // the top runs take the ceiling
+        // the top runs take the ceiling (unbalanced: maximal runs top-down, for experiments)
+        const int len = balanced ? (rem + left - 1) / left : std::min(maxrun, rem);
         runs.push_back({end - len, len});
         end -= len;
     }
@@ -1052,7 +1053,9 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     if (q->m > qk::KT) {
         int minpass = 3;
         if (const char *e = std::getenv("QSIM_F32_PASSENGERS"); q->f32 && e) minpass = std::max(3, std::min(6, std::atoi(e)));
-        q->sets = build_sets(q->m, (int)q->es, minpass);
+        if (const char *e = std::getenv("QSIM_PASSENGERS")) minpass = std::max(3, std::min(6, std::atoi(e)));
+        const char *bal = std::getenv("QSIM_RUNS_BALANCED");
+        q->sets = build_sets(q->m, (int)q->es, minpass, !(bal && std::atoi(bal) == 0));
         CK(cudaMalloc(&q->d_rec, qk::TILE_REC_BYTES << (q->m - qk::KT)));
     }
     if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
