@@ -74,6 +74,11 @@ struct PassParams {
     // so that the tiles in flight at one time span all groups (moving passes interleave NVLink
     // and HBM traffic instead of alternating phases of each); 0 = natural order
     int ord_rot, ord_bits;
+    // CTA tile assignment: groups of 2^ord_grp address-adjacent tiles (tile-id bit 0 = physical
+    // bit 3 of a run set) go to one CTA back to back, so the two groups load and store
+    // neighbouring 128-byte rows together; 0 = cyclic (tile k to CTA k mod grid)
+    int ord_grp;
+    int defer;           // turning-run passes: refill a TMA-stored stage one tile later (no store wait)
     int dbg;             // diagnostics (qsim_bench_pass): bit 0 skip stores, bit 1 skip state loads
     int tma_store;       // store tiles with TMA from the stage instead of STG from registers
     int l2hint;          // L2 cache policy: bits 0-1 loads, bits 2-3 stores (0 none, 1 evict_first, 2 evict_last)

@@ -346,6 +346,8 @@ struct qsim {
     int l2promo = (int)CU_TENSOR_MAP_L2_PROMOTION_L2_128B;  // TMA L2 sector promotion (QSIM_L2PROMO=0..3)
     int tma_store = 1;         // TMA stores from the stage (QSIM_TMA_STORE=0: STG from registers)
     int l2hint = 0;            // TMA L2 cache policy (QSIM_L2HINT, see PassParams::l2hint)
+    int ord_grp = 0;           // adjacent-tile groups per CTA for run sets (QSIM_ORD_GRP, PassParams::ord_grp)
+    int defer = 1;             // deferred stage refill after TMA stores (QSIM_DEFER, PassParams::defer)
     std::string err;
     // optional per-pass timing (CUDA events on the handle's stream around each pass launch)
     bool prof = false;
@@ -475,6 +477,8 @@ qk::PassParams base_params(qsim *q, const TileSet &S) {
     P.prefetch = q->prefetch && S.full12;
     P.tma_store = q->tma_store;
     P.l2hint = q->l2hint;
+    P.ord_grp = S.full12 ? 0 : std::min(q->ord_grp, (int)(q->m - qk::KT));
+    P.defer = q->defer;
     return P;
 }
 
@@ -1056,6 +1060,24 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
         if (const char *e = std::getenv("QSIM_PASSENGERS")) minpass = std::max(3, std::min(6, std::atoi(e)));
         const char *bal = std::getenv("QSIM_RUNS_BALANCED");
         q->sets = build_sets(q->m, (int)q->es, minpass, !(bal && std::atoi(bal) == 0));
+        // Split runs (one GPU, two 9-bit runs, i.e. m = 30): run 1 takes the bits [12, 12+a) and
+        // the top 9-a bits, run 2 the 9 bits between.  With 128-byte rows a run on the top
+        // bits [21, 30) streams at 61-69 % of HBM even for reads alone (the run on [12, 21) at
+        // 97 %); with a = 4 both runs stream like the low one (passbench, profiles/r1_runsplit.txt).
+        // QSIM_RUNSPLIT=a overrides a (0 = contiguous runs).
+        int split_a = 4;
+        if (const char *e = std::getenv("QSIM_RUNSPLIT")) split_a = std::max(0, std::min(8, std::atoi(e)));
+        if (split_a > 0 && world == 1 && q->sets.size() == 3 && q->m == qk::KT + 18) {
+            const int a = split_a;
+            std::vector<int> L1, L2;
+            for (int i = 0; i < 3; ++i) { L1.push_back(i); L2.push_back(i); }
+            for (int i = 0; i < a; ++i) L1.push_back(qk::KT + i);
+            for (int i = 0; i < 9 - a; ++i) L1.push_back(q->m - (9 - a) + i);
+            for (int i = 0; i < 9; ++i) L2.push_back(qk::KT + a + i);
+            q->sets[1] = make_set(q->m, L1, ((1u << 9) - 1) << 3, (int)q->es);
+            q->sets[2] = make_set(q->m, L2, ((1u << 9) - 1) << 3, (int)q->es);
+            q->sets[1].full12 = q->sets[2].full12 = false;
+        }
         CK(cudaMalloc(&q->d_rec, qk::TILE_REC_BYTES << (q->m - qk::KT)));
     }
     if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
@@ -1168,6 +1190,8 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     if (const char *e = std::getenv("QSIM_L2PROMO")) q->l2promo = std::atoi(e);
     if (const char *e = std::getenv("QSIM_TMA_STORE")) q->tma_store = std::atoi(e);
     if (const char *e = std::getenv("QSIM_L2HINT")) q->l2hint = std::atoi(e);
+    if (const char *e = std::getenv("QSIM_ORD_GRP")) q->ord_grp = std::max(0, std::min(4, std::atoi(e)));
+    if (const char *e = std::getenv("QSIM_DEFER")) q->defer = std::atoi(e) != 0;
     if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
     if (q->use_tma) {
         CK(qk::setup_tma_kernels());

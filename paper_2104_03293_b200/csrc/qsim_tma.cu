@@ -150,10 +150,16 @@ __device__ __forceinline__ u64 tile_of(const PassParams &P, u64 k) {
     return ((k << P.ord_rot) | (k >> (P.ord_bits - P.ord_rot))) & mask;
 }
 
+// global sequence index of the CTA's i-th tile (cyclic over CTAs in groups of 2^ord_grp)
+__device__ __forceinline__ u64 seq_of(const PassParams &P, u64 i) {
+    const int q = P.ord_grp;
+    return ((blockIdx.x + (i >> q) * (u64)gridDim.x) << q) + (i & ((1ull << q) - 1ull));
+}
+
 template <bool MV>
-__device__ __forceinline__ void issue_tile(const PassParams &P, const TmaIssue &I, u64 k, int s, bool load_state,
+__device__ __forceinline__ void issue_tile(const PassParams &P, const TmaIssue &I, u64 i, int s, bool load_state,
                                            bool load_rec) {
-    const u64 ut = tile_of<MV>(P, k);
+    const u64 ut = tile_of<MV>(P, seq_of(P, i));
     const uint32_t bytes = (load_state ? I.tile_bytes : 0u) + (load_rec ? (uint32_t)TILE_REC_BYTES : 0u);
     if (!bytes) {
         I.issued[s] = I.issued[s] + 1;
@@ -250,7 +256,8 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     const int n = P.n;
     const bool need_e = TURN || P.reduce;
     const bool load_state = !(TURN && P.init) && !(P.dbg & 2);
-    const u64 ntl = (P.ntiles > blockIdx.x) ? (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const u64 ngrp = P.ntiles >> P.ord_grp;
+    const u64 ntl = ((ngrp > blockIdx.x) ? (ngrp - blockIdx.x + gridDim.x - 1) / gridDim.x : 0) << P.ord_grp;
     volatile int *issued = reinterpret_cast<volatile int *>(smem + TmaSmem::iss_off);
     const TmaIssue I{&tmap, MV ? &smap : &tmap, reinterpret_cast<const TileRec *>(P.rec), stages, (uint32_t)(TILE * sizeof(V)),
                      srec, full, issued};
@@ -267,7 +274,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     __syncthreads();
     if (tid == 0)
         for (int i = 0; i < NSTAGE && (u64)i < ntl; ++i)
-            issue_tile<MV>(P, I, blockIdx.x + (u64)i * gridDim.x, i, load_state, need_e);
+            issue_tile<MV>(P, I, (u64)i, i, load_state, need_e);
 
     int ft = 0;  // tile-bit flips (X gates of the |tan beta| > 1 mixer form)
 #pragma unroll
@@ -305,9 +312,11 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     const int skE = frame_skew<FE, V>(lane);  // skew of the phase / reduction frame
     double acc_e = 0.0, acc_n = 0.0;
     V v[NR];
+    long long pend = -1;  // tile whose TMA store still reads its stage (deferred refill)
+    int pend_s = 0;
     for (u64 i = g; i < ntl; i += TMA_NG) {
         const int s = (int)(i % NSTAGE);
-        const u64 ut = tile_of<MV>(P, blockIdx.x + i * gridDim.x);
+        const u64 ut = tile_of<MV>(P, seq_of(P, i));
         const u64 tb = tile_base(P, ut);
         V *sm = reinterpret_cast<V *>(stages + (size_t)s * SM_TILE_BYTES);
         const TileRec *R = srec + s;
@@ -324,20 +333,36 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
 #pragma unroll
                 for (int j = 0; j < NR; ++j) v[j] = VT<V>::mk((typename VT<V>::S)P.a0, 0);
             }
+            // deferred refill (P.defer): the TMA store of the group's previous tile is left
+            // running and its stage is refilled after this tile's first frame load, so the
+            // elected thread does not stall its warp (and the group's next barrier) on the store
+            auto refill_pending = [&]() {
+                if (gt == 0 && pend >= 0) {
+                    bulk_wait_read0();
+                    if ((u64)pend + NSTAGE < ntl) issue_tile<MV>(P, I, (u64)pend + NSTAGE, pend_s, load_state, need_e);
+                    pend = -1;
+                }
+            };
+            if (!load_state) refill_pending();
             int prev = -1;  // frame of the registers: 0 = X, 1 = W
+            // frame I/O as compile-time frames (immediate smem offsets; a run-time frame
+            // index cost ~4 integer instructions per element, a quarter of the pass's issue)
 #pragma unroll 1
             for (int stp = load_state ? 0 : 2; stp < 4; ++stp) {
                 const int fr_now = (stp == 1 || stp == 2) ? 1 : 0;
                 if (load_state && fr_now != prev) {
                     if (prev >= 0) {
-                        sts_rt(v, sm, prev ? tWt : tXt, prev ? Frame<FW>::RB : Frame<FX>::RB, prev ? skW : 0);
+                        if (prev) sts_frame<FW>(v, sm, lane, warp);
+                        else sts_frame<FX>(v, sm, lane, warp);
                         group_bar(g);
                     }
-                    lds_rt(v, sm, fr_now ? tWt : tXt, fr_now ? Frame<FW>::RB : Frame<FX>::RB, fr_now ? skW : 0);
+                    if (fr_now) lds_frame<FW>(v, sm, lane, warp);
+                    else lds_frame<FX>(v, sm, lane, warp);
+                    if (prev < 0) refill_pending();
                 } else if (!load_state && stp == 3) {
-                    sts_rt(v, sm, tWt, Frame<FW>::RB, skW);
+                    sts_frame<FW>(v, sm, lane, warp);
                     group_bar(g);
-                    lds_rt(v, sm, tXt, Frame<FX>::RB);
+                    lds_frame<FX>(v, sm, lane, warp);
                 }
                 prev = fr_now;
                 if (stp == 2) apply_phase<FW>(v, R, tE, fr, pconst, u, cs.PRR, cs.PRRf, skW);
@@ -346,7 +371,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                         fence_async_smem();
                         group_bar(g);
                         if (gt == 0 && i + NSTAGE < ntl)
-                            issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                            issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
                     }
                 }
                 mix5(v, stp == 0 ? mx1 : stp == 1 ? mw1 : stp == 2 ? mw2 : mx2, stp < 2 ? P.c1.t : P.c2.t);
@@ -354,15 +379,20 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             if (MV && P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
             else if (P.tmo) store_tile_major<FX>(v, P, ut, lane, warp);
             else if (P.tma_store) {
-                sts_rt(v, sm, tXt, Frame<FX>::RB);
+                sts_frame<FX>(v, sm, lane, warp);
                 fence_async_smem();
                 group_bar(g);
                 if (gt == 0) {
                     int c[5];
                     tile_coords(P, ut, c);
                     tma_store_5d(I.tms, c, sm, (P.l2hint >> 2) & 3);
-                    bulk_wait_read0();
-                    if (i + NSTAGE < ntl) issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                    if (P.defer) {
+                        pend = (long long)i;
+                        pend_s = s;
+                    } else {
+                        bulk_wait_read0();
+                        if (i + NSTAGE < ntl) issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
+                    }
                 }
             } else
                 store_tile<FX>(v, OUTB + tb + offX, P.L);
@@ -419,7 +449,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             fence_async_smem();
             group_bar(g);
             if (gt == 0 && i + NSTAGE < ntl)
-                issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
         }
         // ------------------------------------------------ finish in registers, store
         if (TURN) {
@@ -435,7 +465,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                     tile_coords(P, ut, c);
                     tma_store_5d(I.tms, c, sm, (P.l2hint >> 2) & 3);
                     bulk_wait_read0();
-                    if (i + NSTAGE < ntl) issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                    if (i + NSTAGE < ntl) issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
                 }
             } else
                 store_tile<FX>(v, OUTB + tb + offX, P.L);
@@ -464,7 +494,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                         fence_async_smem();
                         group_bar(g);
                         if (gt == 0 && i + NSTAGE < ntl)
-                            issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                            issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
                     }
                     const u64 wm = ((1ull << P.gbits) - 1ull) << sh;
                     store_tile<RUN ? FW : FZ>(v, reinterpret_cast<V *>(P.dst[vr]) + ((tb & ~wm) | ((u64)P.rank << sh)) + offS,
@@ -481,7 +511,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                     tile_coords(P, ut, c);
                     tma_store_5d(I.tms, c, sm, (P.l2hint >> 2) & 3);
                     bulk_wait_read0();
-                    if (i + NSTAGE < ntl) issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                    if (i + NSTAGE < ntl) issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
                 }
                 continue;
             }
@@ -489,13 +519,14 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 fence_async_smem();
                 group_bar(g);
                 if (gt == 0 && i + NSTAGE < ntl)
-                    issue_tile<MV>(P, I, blockIdx.x + (i + NSTAGE) * gridDim.x, s, load_state, need_e);
+                    issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
             }
             if (P.tmo) store_tile_major<RUN ? FW : FZ>(v, P, ut, lane, warp);
             else store_tile<RUN ? FW : FZ>(v, OUTB + tb + offS, P.L, skE);
         }
         }  // generic body
     }
+    if (pend >= 0) bulk_wait_read0();  // the stage must stay valid until the last store read it
     if (MV && (P.swap_store || P.mv)) __threadfence_system();  // NVLink stores visible before the pass completes
     if (P.reduce) {
 #pragma unroll
