@@ -16,33 +16,100 @@ static_assert(sizeof(TileRec) == TILE_REC_BYTES, "TileRec size");
 
 // ============================================================ per-tile fields (pre-pass)
 // For every tile u of the pass's tile set: h'_i(z_H) (12 tile bits), E_H(z_H) and, for
-// phase passes, their phase factors e^{-i gamma (.)}.  One thread per tile; ~0.1% of a
-// pass's time, and it removes all per-tile serial work from the streaming kernel.
-__global__ void __launch_bounds__(128) tile_fields_kernel(const PassParams P, TileRec *rec) {
+// phase passes, their phase factors e^{-i gamma (.)}.  It removes all per-tile serial work
+// from the streaming kernel.
+//
+// A warp takes 32 consecutive tiles: their labels differ only in the 5 lowest non-tile bits
+// Hlo (tile_base places tile-id bit k at the k-th non-tile position), so the non-tile bits split
+// into Hlo (per lane) and Hhi (common to the warp).  The warp computes once, lanes in parallel,
+//   A_i = h_i + sum_{j in Hhi} J_ij s_j   (every position i),
+//   E_hh = sum_{j in Hhi} s_j (h_j + sum_{k in Hhi, k > j} J_jk s_k),
+// and each lane finishes its tile with the Hlo terms:
+//   h'_i = A_i + sum_{j in Hlo} J_ij s_j,   E_H = E_hh + sum_{j in Hlo} s_j (A_j + sum_{k in Hlo, k > j} J_jk s_k).
+// Every partial sum of dyadic data is exact, so the fields equal field_hprime / eh_term bit for
+// bit (the per-thread form below serves shards with fewer than 5 tile-id bits).
+constexpr int TF_WARPS = 4;
+__global__ void __launch_bounds__(32 * TF_WARPS) tile_fields_kernel(const PassParams P, TileRec *rec) {
     __shared__ double sh[NMAX];
     __shared__ double sJ[NMAX * NMAX];
+    __shared__ double sA[TF_WARPS][NMAX];
     const int n = P.n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) sh[i] = P.hp[i];
     for (int i = threadIdx.x; i < n * n; i += blockDim.x) sJ[i] = P.Jp[i];
     __syncthreads();
-    for (u64 u = blockIdx.x * (u64)blockDim.x + threadIdx.x; u < P.ntiles; u += (u64)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // Hlo: the 5 lowest non-tile local positions
+    int hlo[5];
+    int nlo = 0;
+    for (int b = 0; b < P.m && nlo < 5; ++b)
+        if (!((P.lmask >> b) & 1ull)) hlo[nlo++] = b;
+    if (nlo < 5) {  // fewer than 32 tiles: one thread per tile
+        for (u64 u = blockIdx.x * (u64)blockDim.x + threadIdx.x; u < P.ntiles; u += (u64)gridDim.x * blockDim.x) {
+            const u64 X = (tile_base(P, u) | P.xglob) ^ P.flip;
+            TileRec r;
+            double eh = 0.0;
+            for (int j = 0; j < n; ++j)
+                if (!((P.lmask >> j) & 1ull)) eh += eh_term(sh, sJ, n, j, X, P.lmask);
+            r.e[KT] = eh;
+#pragma unroll
+            for (int i = 0; i < KT; ++i) r.e[i] = field_hprime(sh, sJ, n, P.L[i], X, P.lmask);
+#pragma unroll
+            for (int i = 0; i <= KT; ++i) r.f[i] = P.phase ? expmi(P.gamma * r.e[i]) : make_double2(1.0, 0.0);
+            r.pad = 0.0;
+            rec[u] = r;
+        }
+        return;
+    }
+    u64 lomask = 0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) lomask |= 1ull << hlo[k];
+    const u64 himask = ~(P.lmask | lomask) & ((n >= 64) ? ~0ull : ((1ull << n) - 1ull));  // Hhi (incl. global bits)
+    double *A = sA[warp];
+    for (u64 wb = (blockIdx.x * (u64)TF_WARPS + warp) * 32; wb < P.ntiles; wb += (u64)gridDim.x * TF_WARPS * 32) {
+        const u64 Xw = (tile_base(P, wb) | P.xglob) ^ P.flip;  // Hhi spins common to the warp
+        double ehh = 0.0;
+        for (int i = lane; i < n; i += 32) {
+            const double *row = sJ + i * n;
+            double a = sh[i], t = 0.0;
+            for (int j = 0; j < n; ++j) {
+                if (!((himask >> j) & 1ull)) continue;
+                const double sj = spin(Xw, j);
+                a += row[j] * sj;
+                if (j > i) t += row[j] * sj;
+            }
+            A[i] = a;
+            if ((himask >> i) & 1ull) ehh += spin(Xw, i) * (sh[i] + t);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) ehh += __shfl_xor_sync(0xffffffffu, ehh, o);
+        __syncwarp();
+        const u64 u = wb + lane;
         const u64 X = (tile_base(P, u) | P.xglob) ^ P.flip;
+        double slo[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) slo[k] = spin(X, hlo[k]);
         TileRec r;
-        double eh = 0.0;
-        for (int j = 0; j < n; ++j)
-            if (!((P.lmask >> j) & 1ull)) eh += eh_term(sh, sJ, n, j, X, P.lmask);
+        double eh = ehh;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            double t = A[hlo[k]];
+#pragma unroll
+            for (int k2 = k + 1; k2 < 5; ++k2) t += sJ[hlo[k] * n + hlo[k2]] * slo[k2];
+            eh += slo[k] * t;
+        }
         r.e[KT] = eh;
 #pragma unroll
-        for (int i = 0; i < KT; ++i) r.e[i] = field_hprime(sh, sJ, n, P.L[i], X, P.lmask);
-        if (P.phase) {
+        for (int i = 0; i < KT; ++i) {
+            double e = A[P.L[i]];
 #pragma unroll
-            for (int i = 0; i <= KT; ++i) r.f[i] = expmi(P.gamma * r.e[i]);
-        } else {
-#pragma unroll
-            for (int i = 0; i <= KT; ++i) r.f[i] = make_double2(1.0, 0.0);
+            for (int k = 0; k < 5; ++k) e += sJ[P.L[i] * n + hlo[k]] * slo[k];
+            r.e[i] = e;
         }
+#pragma unroll
+        for (int i = 0; i <= KT; ++i) r.f[i] = P.phase ? expmi(P.gamma * r.e[i]) : make_double2(1.0, 0.0);
         r.pad = 0.0;
-        rec[u] = r;
+        if (u < P.ntiles) rec[u] = r;
+        __syncwarp();
     }
 }
 
@@ -371,8 +438,8 @@ cudaError_t launch_pass(const PassParams &P, int grid, cudaStream_t s) {
 }
 
 cudaError_t launch_tile_fields(const PassParams &P, void *rec, cudaStream_t s) {
-    int grid = (int)std::min<u64>((P.ntiles + 127) / 128, 8192);
-    tile_fields_kernel<<<grid, 128, 0, s>>>(P, reinterpret_cast<TileRec *>(rec));
+    int grid = (int)std::min<u64>((P.ntiles + 32 * TF_WARPS - 1) / (32 * TF_WARPS), 8192);
+    tile_fields_kernel<<<grid, 32 * TF_WARPS, 0, s>>>(P, reinterpret_cast<TileRec *>(rec));
     return cudaGetLastError();
 }
 

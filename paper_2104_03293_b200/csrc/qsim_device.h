@@ -69,6 +69,11 @@ struct PassParams {
     // is stored into rank v's other buffer at (rank | u)); everything else stays local, written
     // out of place to dst[rank].
     int mv, mv_pshift, mv_pbits;
+    // low-bit swap schedule (mv == 3, MV == 2 kernels): the g global bits are exchanged with the
+    // passenger positions [wsh, wsh + g) (wsh = 3 - g); a moving tile's amplitude at local x goes
+    // to rank c = x's bits there, at x with those bits set to this rank (tiles of group
+    // [mv_lo, mv_hi) move, the others are written out of place locally)
+    int wsh;
     unsigned mv_lo, mv_hi;
     // tile visiting order: the CTA's k-th tile is rotl(k, ord_rot) over ord_bits tile-id bits,
     // so that the tiles in flight at one time span all groups (moving passes interleave NVLink

@@ -59,6 +59,10 @@ struct PassOp {
     int mv = 0;
     unsigned lo = 0, hi = 0;
     bool swap_done = false;
+    // low-bit swap schedule: this pass also mixes the swap positions (turning passes and the
+    // final pass on a turning set)
+    bool wmix = false;
+    int gshift = 0;  // low-bit swap: lowest group bit (PassParams::mv_pshift) of a moving pass
 };
 
 // es = bytes per amplitude (16 FP64, 8 FP32)
@@ -176,17 +180,25 @@ struct SwapSplit {
     std::vector<double> weights; // per pass of the layer, boundary pass first
 };
 
+// `lowswap` (G > 1, P >= 3): the single-GPU boustrophedon, with the g global bits exchanged
+// once per layer with passenger positions by the 12-bit set's pass (low-bit swap)
+// `ls_groups` / `ls_first` (low-bit swap): the swap's amplitudes are split into ls_groups groups
+// (tile-id bits of the next turning set's run, `ls_gshift[set]`); the turning pass before the
+// 12-bit set's pass moves groups [0, ls_first), the 12-bit set's pass the rest.
 std::vector<PassOp> build_schedule(int nsets, int g, int p, const double *gam, const double *bet,
-                                   bool first_init, bool fused = false, const SwapSplit *split = nullptr) {
+                                   bool first_init, bool fused = false, const SwapSplit *split = nullptr,
+                                   bool lowswap = false, unsigned ls_groups = 1, unsigned ls_first = 0,
+                                   const int *ls_gshift = nullptr) {
     std::vector<PassOp> ops;
     const int P = nsets;
-    if (g == 0) {
+    if (g == 0 || lowswap) {
         std::vector<int> order;
         order.push_back(P > 1 ? 1 : 0);
         if (P > 1) order.push_back(0);
         for (int i = 2; i < P; ++i) order.push_back(i);
         auto seq = [&](int k, int idx) { return order[(k % 2 == 0) ? idx : P - 1 - idx]; };
         ops.push_back({seq(0, 0), first_init, true, false, 0u, ~0u, 0.0, bet[0], gam[0], false, false, 0, 0});
+        ops.back().wmix = lowswap;
         for (int k = 0; k < p; ++k) {
             for (int idx = 1; idx < P; ++idx) {
                 int s = seq(k, idx);
@@ -194,6 +206,25 @@ std::vector<PassOp> build_schedule(int nsets, int g, int p, const double *gam, c
                     ops.push_back({s, false, true, false, ~0u, ~0u, bet[k], bet[k + 1], gam[k + 1], false, false, k, k + 1});
                 else
                     ops.push_back({s, false, false, false, ~0u, 0u, bet[k], 0.0, 0.0, false, false, k, 0});
+                if (!lowswap) continue;
+                PassOp &o = ops.back();
+                o.wmix = (idx == P - 1);
+                if (s == 0) {  // the 12-bit set's pass completes the layer's swap
+                    const int gs = ls_gshift ? ls_gshift[seq(k, P - 1)] : 0;
+                    o.mv = 3;
+                    o.lo = ls_first;
+                    o.hi = ls_groups;
+                    o.gshift = gs;
+                    o.swap_done = true;
+                    o.swap_fused = true;
+                    if (ls_first > 0) {  // the preceding turning pass moves groups [0, ls_first)
+                        PassOp &t = ops[ops.size() - 1 - (size_t)idx];
+                        t.mv = 3;
+                        t.lo = 0;
+                        t.hi = ls_first;
+                        t.gshift = gs;
+                    }
+                }
             }
         }
     } else {
@@ -304,6 +335,12 @@ struct qsim {
     // traffic; groups = local bits [mv_pshift, mv_pshift + mv_pbits) (the top run below the
     // swapped bits); per-pass weights QSIM_SPLIT_W ("boundary,next,...")
     bool split = false;
+    // low-bit swap schedule (G = 2 with the fused swap, opt-in QSIM_LOWSWAP=1): 2 passes per
+    // layer like one GPU; the global bit is exchanged with passenger position 2 by the 12-bit
+    // set's pass (PassParams::wsh)
+    bool lowswap = false;
+    bool ls_now = false;  // the current apply_layers call runs the low-bit swap schedule (R_x mixers)
+    double ls_share = 0.5;  // share of the swap moved by the turning pass (QSIM_LS_SHARE)
     int mv_pshift = 0, mv_pbits = 0;
     std::vector<double> split_w;
     int cur = 0;                       // which of bufs[] currently holds the state
@@ -384,6 +421,22 @@ int grid_for(const qsim *q, u64 ntiles) {
 }
 
 // physical position of logical qubit qb in permutation state `par`
+// low-bit swap schedule: positions [3-g, 3) <-> [m, n).  Opt-in (QSIM_LOWSWAP=1): measured on
+// 2 B200s at n = 31 it saves the third pass per layer but its swap moves 64-byte chunks (the
+// passenger granularity), which cross NVLink at ~400 GB/s in the pass kernels instead of ~705 for
+// the top-bit schedule's rows: 21.9-22.3 vs 22.4-22.5 ms per layer
+bool lowswap_layout(int m, int g) {
+    const char *e = std::getenv("QSIM_LOWSWAP");
+    return e && std::atoi(e) == 1 && g == 1 && m >= qk::KT + 10 && m <= 32;
+}
+int phys_pos_low(int n, int m, int g, int par, int qb) {
+    (void)n;
+    if (!par || g == 0) return qb;
+    const int w = 3 - g;
+    if (qb >= w && qb < 3) return m + (qb - w);
+    if (qb >= m) return w + (qb - m);
+    return qb;
+}
 int phys_pos(int n, int m, int g, int par, int qb) {
     if (!par || g == 0) return qb;
     if (qb >= m - g && qb < m) return qb + g;  // top local <-> global
@@ -454,7 +507,7 @@ int materialize_plus(qsim *q) {
 qk::PassParams base_params(qsim *q, const TileSet &S) {
     qk::PassParams P{};
     P.f32 = q->f32;
-    P.multi = q->fused_swap ? 1 : 0;
+    P.multi = q->ls_now ? 2 : (q->fused_swap ? 1 : 0);
     P.psi = q->psi;
     P.hp = q->cur_hp;
     P.Jp = q->cur_Jp;
@@ -537,7 +590,8 @@ int finish_reduce(qsim *q, int nparts) {
 // bookkeeping of a swap of positions [m-g, m) <-> [m, n): permutation and flip mask
 void swap_bookkeeping(qsim *q) {
     int newp[qk::NMAX];
-    for (int x = 0; x < q->n; ++x) newp[x] = phys_pos(q->n, q->m, q->g, 1, x);
+    for (int x = 0; x < q->n; ++x)
+        newp[x] = q->ls_now ? phys_pos_low(q->n, q->m, q->g, 1, x) : phys_pos(q->n, q->m, q->g, 1, x);
     relabel(q, newp);
 }
 
@@ -695,8 +749,32 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         sp.ngroups = 1 << q->mv_pbits;
         sp.weights = q->split_w;
     }
+    q->ls_now = q->lowswap && !q->gmats;  // general / Hadamard mixers keep the top-bit schedule
+    std::vector<int> gsh(q->sets.size(), 0);
+    unsigned ls_groups = 1, ls_first = 0;
+    if (q->ls_now) {
+        // groups: up to 4 bits of the lowest run bits of each run set (tile-id bits of the 12-bit
+        // set and of the other turning set)
+        int gb = 4;
+        for (size_t k = 1; k < q->sets.size(); ++k) {
+            const TileSet &T = q->sets[k];
+            int lo = q->m, len = 0;
+            for (int i = 0; i < qk::KT; ++i)
+                if ((T.own >> i) & 1u) {
+                    lo = std::min(lo, T.L[i]);
+                    ++len;
+                }
+            gsh[k] = lo;
+            gb = std::min(gb, len);
+        }
+        ls_groups = 1u << gb;
+        ls_first = (unsigned)std::lround(q->ls_share * ls_groups);
+        ls_first = std::min(ls_first, ls_groups);
+    }
     std::vector<PassOp> ops = build_schedule((int)q->sets.size(), q->g, p, gam, bet, q->pending_plus, q->fused_swap,
-                                             q->split ? &sp : nullptr);
+                                             q->split ? &sp : nullptr, q->ls_now, ls_groups, ls_first, gsh.data());
+    const int ls_gbits = ilog2((int)ls_groups);
+    const unsigned wtile = q->ls_now ? ((1u << q->g) - 1u) << (3 - q->g) : 0u;  // swap positions (tile bits)
     int last_grid = 0;
     for (const PassOp &op : ops) {
         const TileSet &S = q->sets[op.set];
@@ -706,7 +784,12 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         }
         qk::PassParams P = base_params(q, S);
         std::complex<double> k1(1.0, 0.0), k2(1.0, 0.0);
-        const unsigned m1 = op.mix1 & S.own, m2 = op.mix2 & S.own;
+        unsigned own = S.own;
+        if (q->ls_now) {
+            if (op.wmix) own |= wtile;
+            if (S.full12) own &= ~wtile;
+        }
+        const unsigned m1 = op.mix1 & own, m2 = op.mix2 & own;
         P.c1 = mix_coef(op.b1, k1);
         P.c2 = mix_coef(op.b2, k2);
         P.mix1 = m1;
@@ -742,6 +825,16 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
             P.mv_pbits = q->split ? q->mv_pbits : 0;
             P.mv_lo = op.lo;
             P.mv_hi = op.hi;
+            if (op.mv == 3) {
+                P.wsh = 3 - q->g;
+                P.mv_pshift = op.gshift;
+                P.mv_pbits = ls_gbits;
+                if (ls_gbits > 0) {  // visit the tiles group bits first (moving and local tiles interleave)
+                    P.ord_bits = q->m - qk::KT;
+                    const int tpos = op.gshift - __builtin_popcountll(S.lmask & ((1ull << op.gshift) - 1ull));
+                    P.ord_rot = tpos % P.ord_bits;
+                }
+            }
             for (int c = 0; c < q->world; ++c) P.dst[c] = q->peer[q->cur ^ 1][c];
             outbuf = q->bufs[q->cur ^ 1];
             if (op.mv == 1 && P.mv_pbits > 0) {
@@ -782,6 +875,7 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         }
     }
     q->pending_plus = false;
+    q->ls_now = false;
     if (q->gmats) return QSIM_OK;  // J-only frame: <H_C> is recomputed on demand
     return finish_reduce(q, last_grid);
 }
@@ -927,6 +1021,7 @@ int apply_tilemajor(qsim *q, const double *gam, const double *bet, int p) {
         q->tmp = q->bufs[q->cur ^ 1];
     }
     q->pending_plus = false;
+    q->ls_now = false;
     if (q->gmats) return QSIM_OK;  // J-only frame: <H_C> is recomputed on demand
     return finish_reduce(q, last_grid);
 }
@@ -1168,6 +1263,10 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
             // the moving tiles are interleaved with local ones, while the boundary pass pays
             // ~1.7 ms for its per-element STG stores whatever its share: at G = 2 it moves
             // nothing and keeps its TMA stores in place)
+            {
+                q->lowswap = lowswap_layout(q->m, q->g) && q->sets.size() >= 3;
+                if (const char *sh = std::getenv("QSIM_LS_SHARE")) q->ls_share = std::max(0.0, std::min(1.0, std::atof(sh)));
+            }
             q->split_w.clear();
             q->split_w.push_back(world == 2 ? 0.0 : 1.0);
             for (int s2 = (int)q->sets.size() - 2; s2 >= 0; --s2) q->split_w.push_back(1.0);
@@ -1688,7 +1787,8 @@ int qsim_plan_counts(int n, int world, int p, int *passes_out, int *swaps_out, u
         passes = 1;
     } else {
         std::vector<double> z(p, 0.0);
-        auto ops = build_schedule((int)build_sets(m).size(), g, p, z.data(), z.data(), true, g > 0);
+        const int ns = (int)build_sets(m).size();
+        auto ops = build_schedule(ns, g, p, z.data(), z.data(), true, g > 0, nullptr, lowswap_layout(m, g) && ns >= 3);
         passes = (int)ops.size();
         for (auto &o : ops) swaps += (o.swap_after || o.swap_fused) ? 1 : 0;
     }
@@ -1702,7 +1802,9 @@ int qsim_plan_positions(int n, int world, int layers, int *pos_out) {
     int g = ilog2(world);
     if (n < 1 || n > qk::NMAX || g < 0 || world > 8 || layers < 0 || !pos_out) return QSIM_EINVAL;
     int m = n - g;
-    for (int qb = 0; qb < n; ++qb) pos_out[qb] = phys_pos(n, m, g, layers & 1, qb);
+    const bool low = lowswap_layout(m, g) && build_sets(m).size() >= 3;
+    for (int qb = 0; qb < n; ++qb)
+        pos_out[qb] = low ? phys_pos_low(n, m, g, layers & 1, qb) : phys_pos(n, m, g, layers & 1, qb);
     return QSIM_OK;
 }
 

@@ -111,7 +111,9 @@ __device__ inline double energy_point(const double *hp, const double *Jp, int n,
 //   Y: lanes t5..t9,          warps t10,t11, regs t0..t4
 //   Z: lanes t0..t4,          warps t10,t11, regs t5..t9    (12-bit phase / store)
 //   W: lanes t0,t1,t2,t8,t9,  warps t10,t11, regs t3..t7    (run phase / store)
-enum { FX = 0, FY = 1, FZ = 2, FW = 3 };
+//   V: lanes t0,t1,t7,t8,t9,  warps t10,t11, regs t2..t6    (run frame of the low-bit swap
+//      schedule, multi-GPU: the passenger t2 is mixed with the run; lane-skewed)
+enum { FX = 0, FY = 1, FZ = 2, FW = 3, FV = 4 };
 template <int F> struct Frame;
 template <> struct Frame<FX> {
     static constexpr int RB = 7;
@@ -132,12 +134,19 @@ template <> struct Frame<FW> {
     }
 };
 
+template <> struct Frame<FV> {
+    static constexpr int RB = 2;
+    __device__ static int tthr(int lane, int warp) { return (lane & 3) | ((lane >> 2) << 7) | (warp << 10); }
+};
+
 // Lane skew of a frame's register slots in linear shared memory (element t at t * sizeof(V)):
 // slot j of a lane holds register pattern j ^ skew.  FP64 (16 B, 8 lanes per wavefront):
 // frame Y (lanes on t5..t9) skews t0..t2.  FP32 (8 B, 16 lanes per wavefront): Y skews t0..t3;
 // W (lanes t0,t1,t2,t8,t9) skews t3 by lane bit 3 (t8), so each half-warp covers 32 banks.
+// Frame V (lanes t0,t1,t7,..): FP64 skews t2 by t7, FP32 skews t2,t3 by t7,t8.
 template <int F, typename V>
 __device__ __forceinline__ int frame_skew(int lane) {
+    if (F == FV) return sizeof(V) == 16 ? ((lane >> 2) & 1) : ((lane >> 2) & 3);
     if (sizeof(V) == 16) return F == FY ? (lane & 7) : 0;
     return F == FY ? (lane & 15) : (F == FW ? ((lane >> 3) & 1) : 0);
 }

@@ -143,7 +143,7 @@ struct TmaIssue {
 };
 
 // tile id of the CTA's k-th tile (PassParams::ord_rot; multi-GPU moving passes only)
-template <bool MV>
+template <int MV>
 __device__ __forceinline__ u64 tile_of(const PassParams &P, u64 k) {
     if (!MV || !P.ord_rot) return k;
     const u64 mask = (1ull << P.ord_bits) - 1ull;
@@ -156,7 +156,7 @@ __device__ __forceinline__ u64 seq_of(const PassParams &P, u64 i) {
     return ((blockIdx.x + (i >> q) * (u64)gridDim.x) << q) + (i & ((1ull << q) - 1ull));
 }
 
-template <bool MV>
+template <int MV>
 __device__ __forceinline__ void issue_tile(const PassParams &P, const TmaIssue &I, u64 i, int s, bool load_state,
                                            bool load_rec) {
     const u64 ut = tile_of<MV>(P, seq_of(P, i));
@@ -227,6 +227,20 @@ __device__ __forceinline__ void store_tile_swapped(const V (&v)[NR], const PassP
     }
 }
 
+// store with the low-bit swap (PassParams::wsh): the swap bits are lane bits of frame F, so all
+// 32 amplitudes of a thread go to the same rank c (its base pointer is per thread)
+template <int F, typename V>
+__device__ __forceinline__ void store_lowswap(const V (&v)[NR], const PassParams &P, u64 xb, int sk) {
+    const u64 wm = ((1ull << P.gbits) - 1ull) << P.wsh;
+    const unsigned c = (unsigned)((xb >> P.wsh) & ((1ull << P.gbits) - 1ull));
+    V *const base = reinterpret_cast<V *>(P.dst[c]) + ((xb & ~wm) | ((u64)P.rank << P.wsh));
+    store_tile<F>(v, base, P.L, sk);
+}
+__device__ __forceinline__ bool lowswap_moves(const PassParams &P, u64 tb) {
+    const unsigned grp = (unsigned)((tb >> P.mv_pshift) & ((1ull << P.mv_pbits) - 1ull));
+    return grp >= P.mv_lo && grp < P.mv_hi;
+}
+
 // the mixer of a frame: scaled R_x butterflies, or the general per-bit 2x2 (GMIX)
 // mixer modes: GMIX 0 = scaled R_x, 1 = general per-bit 2x2, 2 = Hadamard
 #define MIXF(FR, MASK, WHICH)                                                             \
@@ -238,7 +252,7 @@ __device__ __forceinline__ void store_tile_swapped(const V (&v)[NR], const PassP
 
 // MV: multi-GPU variant (fused / split global-qubit swap stores, tile order rotation); the
 // single-GPU instances compile without that code (it costs ~3 % in the hot loop)
-template <int KIND, int GMIX, typename V, bool MV>
+template <int KIND, int GMIX, typename V, int MV>
 __global__ void __launch_bounds__(TMA_NG * 128, 1)
     tma_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap smap,
                     const PassParams P) {
@@ -250,7 +264,10 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     double *red = reinterpret_cast<double *>(smem + TmaSmem::red_off);
     constexpr bool RUN = (KIND == K_PLAIN_RUN || KIND == K_TURN_RUN);
     constexpr bool TURN = (KIND == K_TURN12 || KIND == K_TURN_RUN);
-    constexpr int FE = RUN ? FW : FZ;
+    // run frame: W, or V in the low-bit swap schedule (MV == 2, the passenger t2 mixes)
+    constexpr int FRN = (MV == 2) ? FV : FW;
+    constexpr unsigned TMR = (MV == 2) ? 0x07Cu : TMW;
+    constexpr int FE = RUN ? FRN : FZ;
 
     const int tid = threadIdx.x, g = tid >> 7, gt = tid & 127, lane = gt & 31, warp = gt >> 5;
     const int n = P.n;
@@ -306,7 +323,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         }
     }
     const u64 offX = thread_offset<FX>(P.L, lane, warp);
-    const u64 offS = thread_offset<RUN ? FW : FZ>(P.L, lane, warp);
+    const u64 offS = thread_offset<RUN ? FRN : FZ>(P.L, lane, warp);
     __syncthreads();
 
     const int skE = frame_skew<FE, V>(lane);  // skew of the phase / reduction frame
@@ -325,10 +342,10 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         // (instruction-cache footprint: one copy of the butterflies, the smem sweeps and the
         // phase, driven by four mix steps X(mix1) W(mix1) [phase] W(mix2) X(mix2))
         if constexpr (KIND == K_TURN_RUN && GMIX == 0) {
-            const int tXt = Frame<FX>::tthr(lane, warp), tWt = Frame<FW>::tthr(lane, warp);
-            const int skW = frame_skew<FW, V>(lane);
-            const unsigned mx1 = (P.mix1 & TMX) >> 7, mw1 = (P.mix1 & TMW) >> 3;
-            const unsigned mw2 = (P.mix2 & TMW) >> 3, mx2 = (P.mix2 & TMX) >> 7;
+            const int skW = frame_skew<FRN, V>(lane);
+            constexpr int RBW = Frame<FRN>::RB;
+            const unsigned mx1 = (P.mix1 & TMX) >> 7, mw1 = (P.mix1 & TMR) >> RBW;
+            const unsigned mw2 = (P.mix2 & TMR) >> RBW, mx2 = (P.mix2 & TMX) >> 7;
             if (!load_state) {
 #pragma unroll
                 for (int j = 0; j < NR; ++j) v[j] = VT<V>::mk((typename VT<V>::S)P.a0, 0);
@@ -352,20 +369,20 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 const int fr_now = (stp == 1 || stp == 2) ? 1 : 0;
                 if (load_state && fr_now != prev) {
                     if (prev >= 0) {
-                        if (prev) sts_frame<FW>(v, sm, lane, warp);
+                        if (prev) sts_frame<FRN>(v, sm, lane, warp);
                         else sts_frame<FX>(v, sm, lane, warp);
                         group_bar(g);
                     }
-                    if (fr_now) lds_frame<FW>(v, sm, lane, warp);
+                    if (fr_now) lds_frame<FRN>(v, sm, lane, warp);
                     else lds_frame<FX>(v, sm, lane, warp);
                     if (prev < 0) refill_pending();
                 } else if (!load_state && stp == 3) {
-                    sts_frame<FW>(v, sm, lane, warp);
+                    sts_frame<FRN>(v, sm, lane, warp);
                     group_bar(g);
                     lds_frame<FX>(v, sm, lane, warp);
                 }
                 prev = fr_now;
-                if (stp == 2) apply_phase<FW>(v, R, tE, fr, pconst, u, cs.PRR, cs.PRRf, skW);
+                if (stp == 2) apply_phase<FRN>(v, R, tE, fr, pconst, u, cs.PRR, cs.PRRf, skW);
                 if (stp == 3) {  // last smem read done: release the stage unless TMA-storing
                     if (!(P.tma_store && !(MV && P.swap_store) && !P.tmo)) {
                         fence_async_smem();
@@ -376,7 +393,14 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 }
                 mix5(v, stp == 0 ? mx1 : stp == 1 ? mw1 : stp == 2 ? mw2 : mx2, stp < 2 ? P.c1.t : P.c2.t);
             }
-            if (MV && P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
+            if (MV == 2 && P.mv == 3 && lowswap_moves(P, tb)) {  // low-bit swap: per-thread destination
+                if (P.tma_store) {  // the stage is still held (TMA-store mode): release it now
+                    fence_async_smem();
+                    group_bar(g);
+                    if (gt == 0 && i + NSTAGE < ntl) issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
+                }
+                store_lowswap<FX>(v, P, tb + offX, 0);
+            } else if (MV && P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
             else if (P.tmo) store_tile_major<FX>(v, P, ut, lane, warp);
             else if (P.tma_store) {
                 sts_frame<FX>(v, sm, lane, warp);
@@ -404,8 +428,8 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             sts_frame<FX>(v, sm, lane, warp);
             group_bar(g);
             if (RUN) {
-                lds_frame<FW>(v, sm, lane, warp);
-                if (TURN) MIXF(FW, P.mix1 & TMW, 1);
+                lds_frame<FRN>(v, sm, lane, warp);
+                if (TURN) MIXF(FRN, P.mix1 & TMR, 1);
             } else {
                 lds_frame<FY>(v, sm, lane, warp);
                 MIXF(FY, P.mix1 & TMY, 1);
@@ -426,8 +450,8 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             } else if (!(GMIX == 1 && P.gamma == 0.0 && P.scale.x == 1.0 && P.scale.y == 0.0))  // identity phase
                 apply_phase<FE>(v, R, tE, fr, pconst, u, cs.PRR, cs.PRRf, skE);
             if (RUN) {
-                MIXF(FW, P.mix2 & TMW, 2);
-                sts_frame<FW>(v, sm, lane, warp);
+                MIXF(FRN, P.mix2 & TMR, 2);
+                sts_frame<FRN>(v, sm, lane, warp);
                 group_bar(g);
             } else {
                 MIXF(FZ, P.mix2 & TMZ, 2);
@@ -470,7 +494,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             } else
                 store_tile<FX>(v, OUTB + tb + offX, P.L);
         } else {
-            if (RUN) MIXF(FW, P.mix1 & TMW, 1);
+            if (RUN) MIXF(FRN, P.mix1 & TMR, 1);
             else MIXF(FZ, P.mix1 & TMZ, 1);
             if (P.dbg & 1) {  // diagnostics: read-only pass (keep the values alive)
                 double s = 0.0;
@@ -485,6 +509,16 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 for (int j = 0; j < NR; ++j) v[j] = cmul(v[j], sc);
             }
             if (P.reduce) accumulate<FE>(v, R, tE, fr, te, cs.eRR, acc_e, acc_n, skE);
+            if (MV == 2 && P.mv == 3 && lowswap_moves(P, tb)) {  // low-bit swap: per-thread destination
+                if (late_release) {
+                    fence_async_smem();
+                    group_bar(g);
+                    if (gt == 0 && i + NSTAGE < ntl)
+                        issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
+                }
+                store_lowswap<RUN ? FRN : FZ>(v, P, tb + offS, skE);
+                continue;
+            }
             if (MV && P.mv == 1) {  // split swap: this tile may belong to a peer (whole tile moves)
                 const int sh = P.m - P.gbits;
                 const unsigned vr = (unsigned)((tb >> sh) & ((1ull << P.gbits) - 1ull));
@@ -497,13 +531,13 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                             issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
                     }
                     const u64 wm = ((1ull << P.gbits) - 1ull) << sh;
-                    store_tile<RUN ? FW : FZ>(v, reinterpret_cast<V *>(P.dst[vr]) + ((tb & ~wm) | ((u64)P.rank << sh)) + offS,
+                    store_tile<RUN ? FRN : FZ>(v, reinterpret_cast<V *>(P.dst[vr]) + ((tb & ~wm) | ((u64)P.rank << sh)) + offS,
                                               P.L, skE);
                     continue;
                 }
             }
             if (tstore) {
-                sts_frame<RUN ? FW : FZ>(v, sm, lane, warp);
+                sts_frame<RUN ? FRN : FZ>(v, sm, lane, warp);
                 fence_async_smem();
                 group_bar(g);
                 if (gt == 0) {
@@ -521,8 +555,8 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 if (gt == 0 && i + NSTAGE < ntl)
                     issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
             }
-            if (P.tmo) store_tile_major<RUN ? FW : FZ>(v, P, ut, lane, warp);
-            else store_tile<RUN ? FW : FZ>(v, OUTB + tb + offS, P.L, skE);
+            if (P.tmo) store_tile_major<RUN ? FRN : FZ>(v, P, ut, lane, warp);
+            else store_tile<RUN ? FRN : FZ>(v, OUTB + tb + offS, P.L, skE);
         }
         }  // generic body
     }
@@ -554,7 +588,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
 
 size_t tma_smem_bytes() { return TmaSmem::total; }
 
-template <int GMIX, typename V, bool MV>
+template <int GMIX, typename V, int MV>
 cudaError_t setup_tma_kernels_g() {
     const int sh = (int)TmaSmem::total;
     cudaError_t e;
@@ -567,23 +601,26 @@ cudaError_t setup_tma_kernels_g() {
     return cudaFuncSetAttribute(tma_pass_kernel<K_TURN_RUN, GMIX, V, MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
 }
 
-template <typename V, bool MV>
+template <typename V, int MV>
 cudaError_t setup_tma_kernels_v() {
     cudaError_t e = setup_tma_kernels_g<0, V, MV>();
+    if (MV == 2) return e;  // the low-bit swap schedule runs R_x mixers only
     if (e == cudaSuccess) e = setup_tma_kernels_g<1, V, MV>();
     if (e == cudaSuccess) e = setup_tma_kernels_g<2, V, MV>();
     return e;
 }
 
 cudaError_t setup_tma_kernels() {
-    cudaError_t e = setup_tma_kernels_v<double2, false>();
-    if (e == cudaSuccess) e = setup_tma_kernels_v<double2, true>();
-    if (e == cudaSuccess) e = setup_tma_kernels_v<float2, false>();
-    if (e == cudaSuccess) e = setup_tma_kernels_v<float2, true>();
+    cudaError_t e = setup_tma_kernels_v<double2, 0>();
+    if (e == cudaSuccess) e = setup_tma_kernels_v<double2, 1>();
+    if (e == cudaSuccess) e = setup_tma_kernels_v<double2, 2>();
+    if (e == cudaSuccess) e = setup_tma_kernels_v<float2, 0>();
+    if (e == cudaSuccess) e = setup_tma_kernels_v<float2, 1>();
+    if (e == cudaSuccess) e = setup_tma_kernels_v<float2, 2>();
     return e;
 }
 
-template <int GMIX, typename V, bool MV>
+template <int GMIX, typename V, int MV>
 cudaError_t launch_tma_pass_g(const CUtensorMap &tm, const CUtensorMap &sm, const PassParams &P, int grid,
                               cudaStream_t s) {
     const size_t sh = TmaSmem::total;
@@ -597,24 +634,28 @@ cudaError_t launch_tma_pass_g(const CUtensorMap &tm, const CUtensorMap &sm, cons
     return cudaGetLastError();
 }
 
-template <typename V, bool MV>
+template <typename V, int MV>
 cudaError_t launch_tma_pass_v(const CUtensorMap &tm, const CUtensorMap &sm, const PassParams &P, int grid,
                               cudaStream_t s) {
+    if (MV == 2) return P.gmix == 0 ? launch_tma_pass_g<0, V, 2>(tm, sm, P, grid, s) : cudaErrorInvalidValue;
     switch (P.gmix) {
         case 0: return launch_tma_pass_g<0, V, MV>(tm, sm, P, grid, s);
-        case 1: return launch_tma_pass_g<1, V, MV>(tm, sm, P, grid, s);
-        case 2: return launch_tma_pass_g<2, V, MV>(tm, sm, P, grid, s);
+        case 1: return launch_tma_pass_g<1, V, (MV == 2 ? 1 : MV)>(tm, sm, P, grid, s);
+        case 2: return launch_tma_pass_g<2, V, (MV == 2 ? 1 : MV)>(tm, sm, P, grid, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
-// multi-GPU handles (P.multi) launch the MV instances for every pass
+// multi-GPU handles (P.multi) launch the MV instances for every pass: 1 = top-bit swap
+// schedules, 2 = the low-bit swap schedule (run frame V)
 cudaError_t launch_tma_pass(const CUtensorMap &tm, const CUtensorMap &sm, const PassParams &P, int grid,
                             cudaStream_t s) {
-    if (P.f32) return P.multi ? launch_tma_pass_v<float2, true>(tm, sm, P, grid, s)
-                              : launch_tma_pass_v<float2, false>(tm, sm, P, grid, s);
-    return P.multi ? launch_tma_pass_v<double2, true>(tm, sm, P, grid, s)
-                   : launch_tma_pass_v<double2, false>(tm, sm, P, grid, s);
+    if (P.f32) return P.multi == 2 ? launch_tma_pass_v<float2, 2>(tm, sm, P, grid, s)
+                      : P.multi ? launch_tma_pass_v<float2, 1>(tm, sm, P, grid, s)
+                                : launch_tma_pass_v<float2, 0>(tm, sm, P, grid, s);
+    return P.multi == 2 ? launch_tma_pass_v<double2, 2>(tm, sm, P, grid, s)
+           : P.multi ? launch_tma_pass_v<double2, 1>(tm, sm, P, grid, s)
+                     : launch_tma_pass_v<double2, 0>(tm, sm, P, grid, s);
 }
 
 }  // namespace qk

@@ -94,16 +94,19 @@ def test_plan_small_state_single_launch(Q):
     assert Q.qsim_plan_counts(12, 1, 5)[0] == 1
 
 
-@pytest.mark.parametrize("n,world", [(18, 2), (33, 2), (33, 4), (33, 8), (36, 8)])
+@pytest.mark.parametrize("n,world", [(18, 2), (31, 2), (33, 2), (34, 2), (33, 4), (33, 8), (36, 8)])
 def test_plan_multi_gpu_transfer_law(Q, n, world):
     """One swap per layer; each rank sends (G-1)/G of its shard per swap (SURVEY §4 ledger law)."""
     g = world.bit_length() - 1
     m = n - g
     P = 1 + -(-(m - 12) // 9)
+    # top-bit swap schedule: P passes per layer + a trailing pass.  Opt-in low-bit swap schedule
+    # (QSIM_LOWSWAP=1; G = 2 with 22 <= m <= 32): the single-GPU boustrophedon, (P-1) p + 1 passes
+    low = os.environ.get("QSIM_LOWSWAP") == "1" and world == 2 and 22 <= m <= 32
     for p in (1, 3):
         passes, swaps, amps = Q.qsim_plan_counts(n, world, p)
         assert swaps == p
-        assert passes == P * p + 1
+        assert passes == ((P - 1) * p + 1 if low else P * p + 1)
         assert amps * world == (world - 1) * (1 << m)
 
 
@@ -142,3 +145,19 @@ def test_create_rejects_bad_arguments(Q):
     with pytest.raises(Q.QsimError) as ei:
         Q.qsim_create(0)
     assert ei.value.code == Q.QSIM_EINVAL
+
+
+def test_plan_low_bit_swap(Q, monkeypatch):
+    """Opt-in low-bit swap schedule (G = 2, m >= 22): the global qubit is exchanged with passenger
+    position 2 once per layer, 2 passes per layer as on one GPU."""
+    monkeypatch.setenv("QSIM_LOWSWAP", "1")
+    n = 31
+    p1 = Q.qsim_plan_positions(n, 2, 1)
+    assert p1[2] == 30 and p1[30] == 2
+    assert [p1[i] for i in range(n) if i not in (2, 30)] == [i for i in range(n) if i not in (2, 30)]
+    assert Q.qsim_plan_positions(n, 2, 2) == list(range(n))
+    for p in (1, 4):
+        passes, swaps, amps = Q.qsim_plan_counts(n, 2, p)
+        assert passes == 2 * p + 1 and swaps == p and amps * 2 == 1 << 30
+    monkeypatch.delenv("QSIM_LOWSWAP")
+    assert Q.qsim_plan_positions(n, 2, 1)[29] == 30  # default: top local bit <-> global

@@ -6,6 +6,9 @@
 //   bulk     : cp.async.bulk global->smem, then cp.async.bulk smem->peer global (TMA engine)
 //   ce       : cudaMemcpyPeerAsync (copy engines)
 //   local    : st16 into the local second buffer (HBM copy reference)
+//   splitS   : 16-byte stores, chunks of S bytes alternate between the peer and the local second
+//              buffer (the low-bit global-qubit swap: S = 64 / 32 / 16 B at G = 2 / 4 / 8);
+//              GBps_per_dir counts the peer half only
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/p2p_probe tools/p2p_probe.cu
 #include <cuda_runtime.h>
 #include <cstdio>
@@ -36,6 +39,16 @@ __global__ void st16row(const double2 *__restrict__ src, double2 *__restrict__ d
         const size_t t = row >> 9, r = row & 511;
         const size_t drow = r * (rows >> 9) + t;
         __stcs(dst + drow * 8 + e, __ldcs(src + i));
+    }
+}
+
+template <int LOGC>  // chunk = 2^LOGC amplitudes
+__global__ void split(const double2 *__restrict__ src, double2 *__restrict__ peer, double2 *__restrict__ loc,
+                      size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const double2 v = __ldcs(src + i);
+        if ((i >> LOGC) & 1) __stcs(peer + i, v);
+        else __stcs(loc + i, v);
     }
 }
 
@@ -125,8 +138,9 @@ int main(int argc, char **argv) {
     }
     const size_t n = bytes / 16;
     const char *names[] = {"st16", "st16row", "bulk32k", "bulk64k", "bulk32k_x2", "ce", "local_st16", "st16_1dir",
-                           "bulk64k_1dir", "ce_1dir"};
-    for (int v = 0; v < 10; ++v) {
+                           "bulk64k_1dir", "ce_1dir", "split64", "split32", "split16", "split128"};
+    for (int v = 0; v < 14; ++v) {
+        if (argc > 2 && v < 10) continue;  // second argument: split variants only
         for (int grid_mul = 1; grid_mul <= ((v == 0 || v == 1 || v == 6) ? 4 : 1); grid_mul *= 2) {
             float best = 1e30f;
             for (int rep = 0; rep < 4; ++rep) {
@@ -151,6 +165,10 @@ int main(int argc, char **argv) {
                         case 4: bulk<32768><<<sms * 2, 32, 2 * 32768, st[d]>>>((const char *)src[d], (char *)to, bytes); break;
                         case 5:
                         case 9: CK(cudaMemcpyPeerAsync(to, d ^ 1, src[d], d, bytes, st[d])); break;
+                        case 10: split<2><<<sms * 2, 512, 0, st[d]>>>(src[d], to, loc[d], n); break;
+                        case 11: split<1><<<sms * 2, 512, 0, st[d]>>>(src[d], to, loc[d], n); break;
+                        case 12: split<0><<<sms * 2, 512, 0, st[d]>>>(src[d], to, loc[d], n); break;
+                        case 13: split<3><<<sms * 2, 512, 0, st[d]>>>(src[d], to, loc[d], n); break;
                     }
                     CK(cudaGetLastError());
                     CK(cudaEventRecord(e1[d], st[d]));
@@ -167,7 +185,7 @@ int main(int argc, char **argv) {
                 if (rep > 0 && ms < best) best = ms;
             }
             printf("{\"variant\": \"%s\", \"grid_mul\": %d, \"bytes\": %zu, \"ms\": %.3f, \"GBps_per_dir\": %.1f}\n",
-                   names[v], grid_mul, bytes, best, bytes / (best * 1e-3) / 1e9);
+                   names[v], grid_mul, bytes, best, (v >= 10 ? 0.5 : 1.0) * bytes / (best * 1e-3) / 1e9);
         }
     }
     return 0;
