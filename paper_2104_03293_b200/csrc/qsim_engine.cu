@@ -776,6 +776,11 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
     const int ls_gbits = ilog2((int)ls_groups);
     const unsigned wtile = q->ls_now ? ((1u << q->g) - 1u) << (3 - q->g) : 0u;  // swap positions (tile bits)
     int last_grid = 0;
+    // the scaled butterflies' pass-wide scalars kappa^m are global factors: the plain passes'
+    // ones ride on the next phase (turning) or reducing pass, which multiplies anyway, so the
+    // plain passes do no per-amplitude scaling (QSIM_CARRY=0 restores per-pass scaling)
+    std::complex<double> carry(1.0, 0.0);
+    const bool carry_on = !q->gmats && !(std::getenv("QSIM_CARRY") && std::atoi(std::getenv("QSIM_CARRY")) == 0);
     for (const PassOp &op : ops) {
         const TileSet &S = q->sets[op.set];
         {
@@ -795,6 +800,15 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         P.mix1 = m1;
         P.mix2 = op.phase ? m2 : 0u;
         std::complex<double> sc = cpow_int(k1, __builtin_popcount(P.mix1)) * cpow_int(k2, __builtin_popcount(P.mix2));
+        if (carry_on) {  // a plain pass defers its scalar to the next phase or reducing pass
+            if (!op.phase && !op.reduce) {
+                carry *= sc;
+                sc = 1.0;
+            } else {
+                sc *= carry;
+                carry = 1.0;
+            }
+        }
         P.scale = make_double2(sc.real(), sc.imag());
         set_gmix(q, P, S.L, op);
         // X gates of the |tan beta| > 1 form -> flip mask (energies of this pass use the
@@ -1852,11 +1866,16 @@ int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     int grid = 0;
-    rc = launch_pass_any(q, S, P, &grid);  // warm-up
+    // QSIM_BENCH_OOP=1: out of place (TMA stores into a second buffer, same layout) -- probe of
+    // the DRAM read/write mix of in-place vs ping-pong passes
+    double2 *oop = nullptr;
+    if (const char *e = std::getenv("QSIM_BENCH_OOP"); e && std::atoi(e) == 1 && !tm)
+        CK(cudaMalloc(&oop, q->es << q->m));
+    rc = launch_pass_any(q, S, P, &grid, oop);  // warm-up
     if (rc) return rc;
     CK(cudaEventRecord(e0, q->st));
     for (int r = 0; r < reps; ++r) {
-        rc = launch_pass_any(q, S, P, &grid);
+        rc = launch_pass_any(q, S, P, &grid, oop);
         if (rc) return rc;
     }
     CK(cudaEventRecord(e1, q->st));
@@ -1865,6 +1884,7 @@ int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
     CK(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (oop) cudaFree(oop);
     q->res_valid = false;
     *ms_out = ms / reps;
     return QSIM_OK;
