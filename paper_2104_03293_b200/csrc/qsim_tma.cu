@@ -29,7 +29,10 @@ struct TmaSmem {
     static constexpr size_t iss_off = bar_off + 32;  // int issued[NSTAGE]
     static constexpr size_t cs_off = bar_off + 64;
     static constexpr size_t red_off = cs_off + ((sizeof(CtaShared) + 15) / 16) * 16;
-    static constexpr size_t total = red_off + 2 * 8 * TMA_NG * 4;
+    // per-thread phase constants of the turning-run body (u[0..4], pconst), [slot][thread]:
+    // kept out of the register file, which holds the tile (they caused ~200 B of spills)
+    static constexpr size_t uc_off = red_off + 2 * 8 * TMA_NG * 4;
+    static constexpr size_t total = uc_off + 6 * TMA_NG * 128 * sizeof(double2);
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -322,6 +325,12 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             cs.PRRf[tid] = vcast<float2>(cs.PRR[tid]);
         }
     }
+    if constexpr (KIND == K_TURN_RUN && GMIX == 0) {
+        double2 *uc = reinterpret_cast<double2 *>(smem + TmaSmem::uc_off) + tid;
+#pragma unroll
+        for (int r = 0; r < 5; ++r) uc[r * TMA_NG * 128] = u[r];
+        uc[5 * TMA_NG * 128] = pconst;
+    }
     const u64 offX = thread_offset<FX>(P.L, lane, warp);
     const u64 offS = thread_offset<RUN ? FRN : FZ>(P.L, lane, warp);
     __syncthreads();
@@ -382,7 +391,13 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                     lds_frame<FX>(v, sm, lane, warp);
                 }
                 prev = fr_now;
-                if (stp == 2) apply_phase<FRN>(v, R, tE, fr, pconst, u, cs.PRR, cs.PRRf, skW);
+                if (stp == 2) {
+                    const double2 *uc = reinterpret_cast<const double2 *>(smem + TmaSmem::uc_off) + tid;
+                    double2 uu[5];
+#pragma unroll
+                    for (int r = 0; r < 5; ++r) uu[r] = uc[r * TMA_NG * 128];
+                    apply_phase<FRN>(v, R, tE, fr, uc[5 * TMA_NG * 128], uu, cs.PRR, cs.PRRf, skW);
+                }
                 if (stp == 3) {  // last smem read done: release the stage unless TMA-storing
                     if (!(P.tma_store && !(MV && P.swap_store) && !P.tmo)) {
                         fence_async_smem();
