@@ -84,6 +84,10 @@ struct PassParams {
     // neighbouring 128-byte rows together; 0 = cyclic (tile k to CTA k mod grid)
     int ord_grp;
     int defer;           // turning-run passes: refill a TMA-stored stage one tile later (no store wait)
+    // e^{-i gamma E_RR(j ^ fr)} of the turning-run phase frame's 32 register patterns, computed on
+    // the host (FP64 R_x turning-run passes of the single-GPU and top-bit schedules): read from
+    // the constant bank instead of shared memory
+    double2 PRR[NR];
     int dbg;             // diagnostics (qsim_bench_pass): bit 0 skip stores, bit 1 skip state loads
     int tma_store;       // store tiles with TMA from the stage instead of STG from registers
     int l2hint;          // L2 cache policy: bits 0-1 loads, bits 2-3 stores (0 none, 1 evict_first, 2 evict_last)

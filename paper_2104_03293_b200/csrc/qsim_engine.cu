@@ -550,6 +550,23 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 // launch one pass: TMA-pipelined kernel (one CTA per SM) or the register-direct kernel
 // `out`: output buffer of an out-of-place pass (TMA stores go there), nullptr = in place
 int launch_pass_any(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, double2 *out = nullptr) {
+    if (P.kind == qk::K_TURN_RUN && P.gmix == 0 && !P.f32 && P.multi != 2) {
+        // pattern factors of the phase frame (W: register bits = tile bits 3..7), the same sums
+        // as err_of<FW> over the current physical frame of J
+        const int n = q->n, RB = 3;
+        int fr = 0;
+        for (int r = 0; r < 5; ++r) fr |= (int)((P.flip >> S.L[RB + r]) & 1ull) << r;
+        for (int j = 0; j < qk::NR; ++j) {
+            const int jj = j ^ fr;
+            double e = 0.0;
+            for (int r = 0; r < 5; ++r)
+                for (int r2 = r + 1; r2 < 5; ++r2)
+                    e += q->J[(size_t)q->qat[S.L[RB + r]] * n + q->qat[S.L[RB + r2]]] * (((jj >> r) & 1) ? 1.0 : -1.0) *
+                         (((jj >> r2) & 1) ? 1.0 : -1.0);
+            const double th = P.gamma * e;
+            P.PRR[j] = make_double2(std::cos(th), -std::sin(th));
+        }
+    }
     if (q->use_tma) {
         auto enc = tmap_encoder();
         if (!enc) return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled unavailable");

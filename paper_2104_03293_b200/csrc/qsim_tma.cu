@@ -396,7 +396,9 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                     double2 uu[5];
 #pragma unroll
                     for (int r = 0; r < 5; ++r) uu[r] = uc[r * TMA_NG * 128];
-                    apply_phase<FRN>(v, R, tE, fr, uc[5 * TMA_NG * 128], uu, cs.PRR, cs.PRRf, skW);
+                    // FP64 frame W has no lane skew: the pattern factors come from the constant bank
+                    apply_phase<FRN>(v, R, tE, fr, uc[5 * TMA_NG * 128], uu,
+                                     (sizeof(V) == 16 && MV != 2) ? P.PRR : cs.PRR, cs.PRRf, skW);
                 }
                 if (stp == 3) {  // last smem read done: release the stage unless TMA-storing
                     if (!(P.tma_store && !(MV && P.swap_store) && !P.tmo)) {
