@@ -6,6 +6,10 @@ import sys
 from collections import defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
+# keep the first kernel's block only (an export may hold several "Kernel Name" sections)
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+if len(starts) > 1:
+    rows = rows[starts[0]:starts[1]]
 hdr = rows[1]
 ix = {k: i for i, k in enumerate(hdr)}
 ex = defaultdict(int)
@@ -15,7 +19,7 @@ tot = 0
 stall_cols = [k for k in hdr if k.startswith("stall_") and "Not Issued" not in k]
 recs = []
 for r in rows[2:]:
-    if len(r) < len(hdr):
+    if len(r) < len(hdr) or not r[ix["Instructions Executed"]].isdigit():
         continue
     src = r[ix["Source"]].strip()
     m = re.match(r"(@!?U?P[T0-9]+\s+)?([A-Z0-9_]+)(\.[A-Z0-9_.]+)?", src)
