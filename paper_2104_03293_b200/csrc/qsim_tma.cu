@@ -340,6 +340,16 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     V v[NR];
     long long pend = -1;  // tile whose TMA store still reads its stage (deferred refill)
     int pend_s = 0;
+    // deferred refill (P.defer): the TMA store of the group's previous tile is left running and
+    // its stage is refilled after this tile's first frame load, so the elected thread does not
+    // stall its warp (and the group's next barrier) on the store
+    auto refill_pending = [&]() {
+        if (gt == 0 && pend >= 0) {
+            bulk_wait_read0();
+            if ((u64)pend + NSTAGE < ntl) issue_tile<MV>(P, I, (u64)pend + NSTAGE, pend_s, load_state, need_e);
+            pend = -1;
+        }
+    };
     for (u64 i = g; i < ntl; i += TMA_NG) {
         const int s = (int)(i % NSTAGE);
         const u64 ut = tile_of<MV>(P, seq_of(P, i));
@@ -359,16 +369,6 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
 #pragma unroll
                 for (int j = 0; j < NR; ++j) v[j] = VT<V>::mk((typename VT<V>::S)P.a0, 0);
             }
-            // deferred refill (P.defer): the TMA store of the group's previous tile is left
-            // running and its stage is refilled after this tile's first frame load, so the
-            // elected thread does not stall its warp (and the group's next barrier) on the store
-            auto refill_pending = [&]() {
-                if (gt == 0 && pend >= 0) {
-                    bulk_wait_read0();
-                    if ((u64)pend + NSTAGE < ntl) issue_tile<MV>(P, I, (u64)pend + NSTAGE, pend_s, load_state, need_e);
-                    pend = -1;
-                }
-            };
             if (!load_state) refill_pending();
             int prev = -1;  // frame of the registers: 0 = X, 1 = W
             // frame I/O as compile-time frames (immediate smem offsets; a run-time frame
@@ -441,6 +441,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         // ------------------------------------------------ rounds up to the last smem read
         if (load_state) {
             lds_frame<FX>(v, sm, lane, warp);
+            refill_pending();
             MIXF(FX, P.mix1 & TMX, 1);
             sts_frame<FX>(v, sm, lane, warp);
             group_bar(g);
@@ -456,6 +457,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 if (TURN) MIXF(FZ, P.mix1 & TMZ, 1);
             }
         } else {
+            refill_pending();
 #pragma unroll
             for (int j = 0; j < NR; ++j) v[j] = VT<V>::mk((typename VT<V>::S)P.a0, 0);
         }
@@ -561,8 +563,13 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                     int c[5];
                     tile_coords(P, ut, c);
                     tma_store_5d(I.tms, c, sm, (P.l2hint >> 2) & 3);
-                    bulk_wait_read0();
-                    if (i + NSTAGE < ntl) issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
+                    if (P.defer) {
+                        pend = (long long)i;
+                        pend_s = s;
+                    } else {
+                        bulk_wait_read0();
+                        if (i + NSTAGE < ntl) issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
+                    }
                 }
                 continue;
             }
