@@ -869,10 +869,11 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
             for (int c = 0; c < q->world; ++c) P.dst[c] = q->peer[q->cur ^ 1][c];
             outbuf = q->bufs[q->cur ^ 1];
             if (op.mv == 1 && P.mv_pbits > 0) {
-                // visit the tiles group bits first (the group bits sit above all 12 tile bits of
-                // a non-boundary set, so they are tile-id bits mv_pshift - 12 ..)
+                // visit the tiles group bits first (the group bits are tile-id bits of every
+                // non-boundary set; their tile-id position = non-tile bits below them)
                 P.ord_bits = q->m - qk::KT;
-                P.ord_rot = (q->mv_pshift - qk::KT) % P.ord_bits;
+                const int tpos = q->mv_pshift - __builtin_popcountll(S.lmask & ((1ull << q->mv_pshift) - 1ull));
+                P.ord_rot = tpos % P.ord_bits;
             }
         }
         if (op.phase || op.reduce) {
@@ -1193,15 +1194,18 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
         // QSIM_RUNSPLIT=a overrides a (0 = contiguous runs).
         int split_a = 4;
         if (const char *e = std::getenv("QSIM_RUNSPLIT")) split_a = std::max(0, std::min(8, std::atoi(e)));
-        if (split_a > 0 && world == 1 && q->sets.size() == 3 && q->m == qk::KT + 18) {
+        // One GPU only: on 2 and 4 GPUs the split layout (top set {12..15, 25..29}, swap groups
+        // on bits 12..15) made the 12-bit pass's share of the swap slower (G = 2: 22.8 vs 22.5 ms
+        // per layer, G = 4: 24.4-27.9 vs 21.7), so the multi-GPU schedules keep contiguous runs.
+        if (split_a > 0 && split_a <= 6 && world == 1 && q->sets.size() == 3 && q->m == qk::KT + 18) {
             const int a = split_a;
             std::vector<int> L1, L2;
             for (int i = 0; i < 3; ++i) { L1.push_back(i); L2.push_back(i); }
             for (int i = 0; i < a; ++i) L1.push_back(qk::KT + i);
             for (int i = 0; i < 9 - a; ++i) L1.push_back(q->m - (9 - a) + i);
             for (int i = 0; i < 9; ++i) L2.push_back(qk::KT + a + i);
-            q->sets[1] = make_set(q->m, L1, ((1u << 9) - 1) << 3, (int)q->es);
-            q->sets[2] = make_set(q->m, L2, ((1u << 9) - 1) << 3, (int)q->es);
+            q->sets[1] = make_set(q->m, L2, ((1u << 9) - 1) << 3, (int)q->es);
+            q->sets[2] = make_set(q->m, L1, ((1u << 9) - 1) << 3, (int)q->es);
             q->sets[1].full12 = q->sets[2].full12 = false;
         }
         CK(cudaMalloc(&q->d_rec, qk::TILE_REC_BYTES << (q->m - qk::KT)));
@@ -1282,11 +1286,17 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
             // split swap: groups from the top run's bits below the swapped ones
             const TileSet &T = q->sets.back();
             int a_top = q->m;
+            u64 tbits = 0;
             for (int i = 0; i < qk::KT; ++i)
-                if ((T.own >> i) & 1u) a_top = std::min(a_top, T.L[i]);
+                if ((T.own >> i) & 1u) {
+                    a_top = std::min(a_top, T.L[i]);
+                    tbits |= 1ull << T.L[i];
+                }
+            int seg = 0;  // contiguous top-set bits from a_top (a split top run has two segments)
+            while (a_top + seg < q->m && ((tbits >> (a_top + seg)) & 1ull)) ++seg;
             const char *sz = std::getenv("QSIM_SPLIT_SWAP");
             q->mv_pshift = a_top;
-            q->mv_pbits = std::min(10, std::max(0, q->m - q->g - a_top));
+            q->mv_pbits = std::min(std::min(10, seg), std::max(0, q->m - q->g - a_top));
             q->split = q->mv_pbits > 0 && q->sets.size() > 1 && !(sz && std::atoi(sz) == 0);
             // default weights ~ the passes' measured single-GPU times (boundary turning run,
             // plain runs, the 12-bit set)
