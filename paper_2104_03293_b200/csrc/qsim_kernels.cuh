@@ -453,14 +453,25 @@ __device__ __forceinline__ void apply_phase(double2 (&v)[NR], const TileRec *R, 
                                             const double2 (&u)[5], const double2 *PRR, const float2 * = nullptr,
                                             int sk = 0) {
     fr ^= sk;  // slot j holds pattern j ^ sk: its spins are those of (j ^ sk ^ flips)
-    double2 base = cmul(R->f[12], pconst);
+    // base = f_H * pconst * prod over the 7 thread tile bits of f_i^{s_i}, as a product tree
+    // (depth 3 instead of a chain of 8 dependent complex multiplies)
+    double2 fac[8];
+    fac[0] = cmul(R->f[12], pconst);
+    {
+        int k = 1;
 #pragma unroll
-    for (int i = 0; i < KT; ++i) {
-        if (i >= Frame<F>::RB && i < Frame<F>::RB + 5) continue;
-        const double2 fi = R->f[i];
-        const double sg = ((tthr >> i) & 1) ? 1.0 : -1.0;
-        base = cmul(base, make_double2(fi.x, sg * fi.y));
+        for (int i = 0; i < KT; ++i) {
+            if (i >= Frame<F>::RB && i < Frame<F>::RB + 5) continue;
+            const double2 fi = R->f[i];
+            const double sg = ((tthr >> i) & 1) ? 1.0 : -1.0;
+            fac[k++] = make_double2(fi.x, sg * fi.y);
+        }
     }
+#pragma unroll
+    for (int w = 1; w < 8; w <<= 1)
+#pragma unroll
+        for (int a = 0; a < 8; a += 2 * w) fac[a] = cmul(fac[a], fac[a + w]);
+    const double2 base = fac[0];
     double2 g[5];
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
