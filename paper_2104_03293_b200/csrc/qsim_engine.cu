@@ -1298,18 +1298,19 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
             q->mv_pshift = a_top;
             q->mv_pbits = std::min(std::min(10, seg), std::max(0, q->m - q->g - a_top));
             q->split = q->mv_pbits > 0 && q->sets.size() > 1 && !(sz && std::atoi(sz) == 0);
-            // default weights ~ the passes' measured single-GPU times (boundary turning run,
-            // plain runs, the 12-bit set)
-            // (measured on 2 B200s: a non-boundary pass moves its share at almost no cost when
-            // the moving tiles are interleaved with local ones, while the boundary pass pays
-            // ~1.7 ms for its per-element STG stores whatever its share: at G = 2 it moves
-            // nothing and keeps its TMA stores in place)
+            // default weights: equal shares for every pass of the layer (boundary turning run,
+            // plain runs, the 12-bit set).  A non-boundary pass moves its share at almost no cost
+            // when the moving tiles are interleaved with local ones; the boundary pass moves per
+            // element (STG).  An earlier kernel made the boundary pass's STG stores cost ~1.7 ms
+            // whatever its share, so G = 2 used "0,1,1" -- no longer the better choice (below).
             {
                 q->lowswap = lowswap_layout(q->m, q->g) && q->sets.size() >= 3;
                 if (const char *sh = std::getenv("QSIM_LS_SHARE")) q->ls_share = std::max(0.0, std::min(1.0, std::atof(sh)));
             }
+            // (re-measured with the final pass kernels: equal shares are best at G = 2 too,
+            // 20.7-20.9 vs 22.5 ms per layer with "0,1,1"; profiles/r1_mgpu2_split_weights.jsonl)
             q->split_w.clear();
-            q->split_w.push_back(world == 2 ? 0.0 : 1.0);
+            q->split_w.push_back(1.0);
             for (int s2 = (int)q->sets.size() - 2; s2 >= 0; --s2) q->split_w.push_back(1.0);
             if (const char *w = std::getenv("QSIM_SPLIT_W")) {
                 std::vector<double> ws;
