@@ -90,6 +90,45 @@ def test_P1_dense_expm(n, p, seed):
     assert np.max(np.abs(got - ref)) < 1e-13
 
 
+@pytest.mark.parametrize("n,p,seed", [(1, 2, 20), (3, 3, 21), (6, 2, 22), (8, 3, 23)])
+def test_P1_apply_layers_from_arbitrary_state(n, p, seed):
+    """oracle_apply_layers (the continuation entry, which evaluates E(z) on the fly: the
+    etab == NULL branch of oracle_apply_phase) from a random normalised state vs the dense
+    expm product of eq:QAOA_state's factors (order of P:683)."""
+    h, J = inst.random_ising(n, seed)
+    g, b = rand_angles(p, seed)
+    rng = np.random.default_rng(seed)
+    psi0 = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    psi0 /= np.linalg.norm(psi0)
+    E = dense_energies(h, J)
+    HD = dense_HD(n)
+    ref = psi0.copy()
+    for gk, bk in zip(g, b):
+        ref = sla.expm(-1j * bk * HD) @ (np.exp(-1j * gk * E) * ref)
+    got = np.ascontiguousarray(psi0.copy())
+    o.apply_layers(h, J, g, b, got)
+    assert np.max(np.abs(got - ref)) < 1e-13
+
+
+def test_P1_apply_layers_continues_qaoa_state():
+    """apply_layers(qaoa_state(g[:k]), g[k:]) == qaoa_state(g) for every split k (the two
+    entries reach the same |beta, gamma>), and the on-the-fly phase equals the
+    table phase bit for bit (dyadic E, reading R14)."""
+    n, p = 9, 5
+    h, J = inst.random_ising(n, 31)
+    g, b = rand_angles(p, 31)
+    full = o.qaoa_state(h, J, g, b)
+    for k in range(1, p):
+        psi = o.qaoa_state(h, J, g[:k], b[:k])
+        o.apply_layers(h, J, g[k:], b[k:], psi)
+        assert np.max(np.abs(psi - full)) < 1e-14
+    # phase alone: on the fly (etab NULL) vs the closed form e^{-i gamma E} psi
+    psi = o.init_plus(n)
+    o.apply_phase(h, J, 0.731, psi)
+    ref = np.exp(-1j * 0.731 * dense_energies(h, J)) * 2.0 ** (-n / 2)
+    assert np.max(np.abs(psi - ref)) < 1e-15
+
+
 def test_P1_layer_order_matters():
     # a swapped order (mixer before phase) must NOT match -> the pin can see it
     h, J = inst.random_ising(4, 7)
