@@ -6,7 +6,17 @@ One "step" = one full AQA evaluation: |+>^n, p layers of e^{-i gamma_k H_C} then
 e^{-i beta_k H_D} (eq:QAOA_state, angles eq:beta_k / eq:gamma_k), <H_C> and P_success.
 Workload (weak scaling): n = 30 + log2(N) qubits on N GPUs (2^30 amplitudes = 17.2 GB per
 GPU), exact-cover-shaped instance (N x 472, seed 0, paper's 30(0)-like, r ~ 37), synthetic
-DW-like schedule, tau = 0.4 ns, p = 32 (BASELINE configs[2] at N=1, configs[3] at N=8).
+DW-like schedule, p = 32, tau = 0.02 ns (BASELINE configs[2] at N=1, configs[3] at N=8).  tau:
+at the paper's 0.4 ns this synthetic schedule sits in the Trotter-breakdown regime
+(P_success ~ 2^-n); 0.02 ns anneals (oracle: P = 0.58 at n = 16, 0.30 at n = 20,
+profiles/r2_tau_scan.txt), so the printed P_success is a meaningful sanity value.  The
+per-layer cost does not depend on tau.
+
+The JSON line also carries the other BASELINE configs as timed extras (N = 1: n = 12 AQA p = 5
+and the 64 x 64 QAOA p = 1 grid, n = 24 QAOA p = 1..10, n = 33 AQA on one GPU; N > 1: n = 33
+over the N GPUs), a per-pass-program roofline (turning run, plain run, 12-bit passes) against
+the measured copy peak and the north star's 8 TB/s, and the algorithmic (one pass per layer)
+fraction.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--p P]
 
@@ -41,12 +51,17 @@ def parse():
     ap.add_argument("--p", type=int, default=32)
     ap.add_argument("--nlocal", type=int, default=30, help="qubits per GPU shard (n = nlocal + log2 N)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the timed extra BASELINE configs")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
                     help="amplitude precision (fp64 = the north-star path; fp32 = the NEXT-4 mode)")
     return ap.parse_args()
 
 
-def workload(n: int, p: int):
+TAU = 0.02  # ns per step (see the module docstring)
+NORTH_STAR_HBM = 8000.0  # GB/s, BASELINE.json north_star's "about 8 TB/s per GPU"
+
+
+def workload(n: int, p: int, tau: float = TAU):
     from paper_2104_03293_b200 import instances as inst
     from paper_2104_03293_b200 import problems as pp
 
@@ -54,7 +69,6 @@ def workload(n: int, p: int):
     h, J, C = pp.ising_from_exact_cover(a)
     r = pp.rescale_r(h, J)
     s, A, B = inst.dw_like_schedule()
-    tau = 0.4  # ns
     # angular units: 2 pi GHz; the rescale 1/r is folded into B (gamma/r, reading R6)
     A_ang = 2 * np.pi * A
     B_ang = 2 * np.pi * B / r
@@ -122,6 +136,183 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def host_info():
+    """CPU model, sockets, logical CPUs and RAM of the box (for the cpu_baseline record)."""
+    info = {"logical_cpus": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip().lower().replace(" ", "_").replace("(s)", "s")] = v.strip()
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal:"):
+                info["ram_gb"] = round(int(line.split()[1]) * 1024 / 1e9, 1)
+    except Exception:
+        pass
+    return info
+
+
+PASS_NAMES = {0: "12-bit plain", 1: "plain run", 2: "12-bit turning", 3: "turning run"}
+
+
+def pass_roofline(ms, kinds, m, es, peak):
+    """Per pass program: launches, mean duration, algorithmic bytes per launch (read + write of
+    the 2^m-amplitude shard, write only for the |+> init pass) / mean duration, against the
+    measured copy peak and the north star's 8 TB/s; share of the summed pass time."""
+    tot = float(np.sum(ms)) if len(ms) else 1.0
+    out = {}
+    for k, name in PASS_NAMES.items():
+        sel = (kinds & 3) == k
+        if not np.any(sel):
+            continue
+        by = np.where(kinds[sel] & 8, 1.0, 2.0) * es * float(1 << m)
+        t = ms[sel]
+        gbs = float(np.mean(by)) / (float(np.mean(t)) / 1e3) / 1e9
+        out[name] = {"launches": int(sel.sum()), "avg_ms": float(np.mean(t)), "min_ms": float(np.min(t)),
+                     "alg_bytes_per_launch": float(np.mean(by)), "achieved_GBps": gbs,
+                     "frac_measured_peak": gbs / peak, "frac_8TBps": gbs / NORTH_STAR_HBM,
+                     "share_of_pass_time": float(np.sum(t)) / tot,
+                     "moving_launches": int(np.sum((kinds[sel] & 4) != 0))}
+    return out
+
+
+def _timed(stream, fn, reps):
+    import torch
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def extra_configs_single(Q, stream, args):
+    """BASELINE configs[0], [1] and [3] at N = 1 (timed with CUDA events on the library stream;
+    each sample = the named workload through the public C-ABI, results synchronised)."""
+    from paper_2104_03293_b200 import instances as inst
+    from paper_2104_03293_b200 import problems as pp
+
+    res = {}
+    # configs[0]: n = 12 planted 2-SAT, AQA p = 5 (toy schedule) + the 64 x 64 QAOA p = 1 grid
+    n = 12
+    clauses, _ = inst.planted_2sat(n, seed=0)
+    h, J, _C = pp.ising_from_2sat(n, clauses)
+    s_, A, B = inst.toy_schedule()
+    with Q.QSim(n, cuda_stream=stream.cuda_stream) as sim:
+        sim.set_ising(h, J)
+
+        def aqa():
+            sim.init_plus()
+            sim.apply_aqa(2.5, 5, s_, A, B)
+            return sim.expect_hc()
+
+        aqa()
+        ms = _timed(stream, aqa, 200)
+        betas = np.arange(64) * np.pi / 64
+        gammas = np.arange(64) * 2 * np.pi / 64
+        t0 = time.perf_counter()
+        best = None
+        for bb in betas:
+            for gg in gammas:
+                sim.init_plus()
+                sim.apply_qaoa([gg], [bb])
+                e = sim.expect_hc()
+                best = e if best is None else min(best, e)
+        grid_s = time.perf_counter() - t0
+    res["n12_2sat"] = {"config": "BASELINE configs[0]: n=12 planted 2-SAT, AQA p=5 (A=1-s, B=s, T=2.5) + "
+                                 "64x64 QAOA p=1 grid (beta in [0,pi), gamma in [0,2pi))",
+                       "aqa_us_per_layer": ms * 1e3 / 5, "aqa_us_per_evaluation": ms * 1e3,
+                       "grid_evaluations_per_s": 4096 / grid_s, "grid_best_expect_hc": best,
+                       "note": "one small_kernel launch per evaluation (whole state in one CTA); "
+                               "per-evaluation time includes the <H_C> read-back sync"}
+    # configs[1]: n = 24 dense Ising, QAOA p = 1..10, fixed angle schedule
+    n = 24
+    h, J = inst.random_ising(n, 1)
+    per = []
+    with Q.QSim(n, cuda_stream=stream.cuda_stream) as sim:
+        sim.set_ising(h, J)
+        for p in range(1, 11):
+            k = np.arange(1, p + 1)
+            gam = 0.8 * k / (p + 1)
+            bet = -0.6 * (1 - k / (p + 1))
+
+            def run():
+                sim.init_plus()
+                sim.apply_qaoa(gam, bet)
+                return sim.expect_hc()
+
+            run()
+            ms = _timed(stream, run, 10)
+            per.append({"p": p, "ms_per_evaluation": ms, "ms_per_layer": ms / p,
+                        "layer_amp_updates_per_s": (1 << n) * p / (ms / 1e3), "expect_hc": run()})
+    res["n24_qaoa"] = {"config": "BASELINE configs[1]: n=24 dense Ising (seed 1), QAOA p=1..10, "
+                                 "gamma_k=0.8k/(p+1), beta_k=-0.6(1-k/(p+1)); evaluation = |+> + p layers + <H_C>",
+                       "per_p": per}
+    # configs[3] at N = 1: n = 33 AQA on one GPU (137 GB state)
+    import torch
+
+    n, p = 33, args.p
+    if torch.cuda.mem_get_info()[0] > (16 << n) + (4 << 30):
+        w = workload(n, p)
+        with Q.QSim(n, cuda_stream=stream.cuda_stream) as sim:
+            sim.set_ising(w["h"], w["J"])
+
+            def step():
+                sim.init_plus()
+                sim.apply_aqa(w["T"], p, w["s"], w["A"], w["B"])
+                return sim.expect_hc(), sim.success_prob([w["z_star"]])
+
+            step()
+            ms = _timed(stream, step, 2)
+            e, ps = step()
+        res["n33_1gpu"] = {"config": f"BASELINE configs[3] on one GPU: n=33 AQA p={p} exact-cover-shaped, "
+                                     f"tau={TAU} ns", "ms_per_step": ms, "sec_per_layer": ms / 1e3 / p,
+                           "layer_amp_updates_per_s": (1 << n) * p / (ms / 1e3),
+                           "alg_frac_measured_peak": 32.0 * (1 << n) / (ms / 1e3 / p) / 1e9 / peaks()[0],
+                           "expect_hc_plus_C": e + w["C"], "p_success": ps}
+    else:
+        res["n33_1gpu"] = {"skipped": "not enough free device memory"}
+    return res
+
+
+def extra_config_multi(Q, stream, args, world, rank, uid_fn):
+    """BASELINE configs[3] over the N GPUs of this run: n = 33 AQA p (strong scaling against the
+    n33_1gpu extra of the N = 1 line), device time max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    n, p = 33, args.p
+    w = workload(n, p)
+    sim = Q.QSim(n, rank=rank, world=world, nccl_unique_id=uid_fn(), cuda_stream=stream.cuda_stream)
+    sim.set_ising(w["h"], w["J"])
+
+    def step():
+        sim.init_plus()
+        sim.apply_aqa(w["T"], p, w["s"], w["A"], w["B"])
+        return sim.expect_hc(), sim.success_prob([w["z_star"]])
+
+    step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = _timed(stream, step, 2)
+    t = torch.tensor([ms], dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    e, ps = step()
+    path = sim.swap_path
+    sim.close()
+    return {"n33_sharded": {"config": f"BASELINE configs[3]: n=33 AQA p={p} over {world} GPUs (strong scaling)",
+                            "ms_per_step": ms, "sec_per_layer": ms / 1e3 / p,
+                            "layer_amp_updates_per_s": (1 << n) * p / (ms / 1e3), "swap_path": path,
+                            "expect_hc_plus_C": e + w["C"], "p_success": ps}}
+
+
 def cpu_baseline(nlocal_sample: int = 26, p_sample: int = 2):
     """The oracle as it stands, on a bounded sample of the same workload (same generator and
     schedule, n = nlocal_sample, p_sample layers), timed on the host cores."""
@@ -135,7 +326,7 @@ def cpu_baseline(nlocal_sample: int = 26, p_sample: int = 2):
     ps = o.success_prob(psi, [w["z_star"]])
     dt = time.perf_counter() - t0
     value = (1 << nlocal_sample) * p_sample / dt
-    return {"value": value, "unit": UNIT, "cores": o.num_threads(), "kind": "oracle",
+    return {"value": value, "unit": UNIT, "cores": o.num_threads(), "kind": "oracle", "host": host_info(),
             "sample": f"oracle.aqa_state + expect_hc + success_prob at n={nlocal_sample}, p={p_sample} "
                       f"(same generator/schedule), {dt:.2f} s", "seconds": dt, "expect_hc": e, "p_success": ps}
 
@@ -165,7 +356,7 @@ def run_reference(args):
             "config": {"workload": f"AQA exact-cover-shaped, bounded CPU sample n={n_s} p={p_s} of the "
                                    f"n={args.nlocal}+log2(N) p={args.p} workload", "n": n_s, "p": p_s},
             "cpu_baseline": {"value": value, "unit": UNIT, "kind": "oracle", "cores": o.num_threads(),
-                             "sample": f"n={n_s}, p={p_s} per step"},
+                             "sample": f"n={n_s}, p={p_s} per step", "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -194,11 +385,13 @@ def main():
     n = args.nlocal + g
     p = args.p
     w = workload(n, p)
-    uid = None
-    if world > 1:
+    def uid_fn():
+        """a fresh ncclUniqueId per handle, created on rank 0 and broadcast"""
         obj = [Q.qsim_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+        return obj[0]
+
+    uid = uid_fn() if world > 1 else None
     # a dedicated stream: the library enqueues every kernel on it and the timing events are
     # recorded on it (torch's default stream is the legacy null stream, handle 0)
     stream = torch.cuda.Stream(dev)
@@ -237,8 +430,10 @@ def main():
     ev1.record(stream)
     barrier()
     ms = ev0.elapsed_time(ev1)
-    pass_ms, pass_cnt, pass_bytes = Q.qsim_profile_read(sim.h)
+    pass_list, pass_kinds = Q.qsim_profile_passes(sim.h, cap=1 << 16, kinds=True)
     Q.qsim_profile_enable(sim.h, False)
+    pass_ms = float(np.sum(pass_list))
+    pass_cnt = len(pass_list)
     launches = sim.launches - launches0
     clocks = clk.stop()
     t = torch.tensor([ms, pass_ms], dtype=torch.float64, device=dev)
@@ -266,26 +461,43 @@ def main():
     h2d = h_host.nbytes + J_host.nbytes + 3 * w["s"].nbytes + 8
     d2h = 16 + 16
 
+    peak, peak_src = peaks()
+    m = args.nlocal
+    per_kind = pass_roofline(pass_list, pass_kinds, m, es, peak)
+    # the dominant pass program (largest share of the pass time) is the roofline line's kernel
+    dom = max(per_kind, key=lambda k: per_kind[k]["share_of_pass_time"])
+    t_layer = ms_step / 1e3 / p
+    alg = {"bytes_per_layer": 2.0 * es * (1 << m), "note": "one read + one write of the shard per layer "
+           "(the 1-pass floor); this build runs (P-1)p+1 passes for p layers on one GPU",
+           "frac_measured_peak": 2.0 * es * (1 << m) / t_layer / 1e9 / peak,
+           "frac_8TBps": 2.0 * es * (1 << m) / t_layer / 1e9 / NORTH_STAR_HBM}
+    sim.close()
+    extras = None
+    if world == 1 and not args.no_extras:
+        extras = extra_configs_single(Q, stream, args)
+    elif world > 1 and not args.no_extras:
+        extras = extra_config_multi(Q, stream, args, world, rank, uid_fn)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline()
     if rank == 0:
-        peak, peak_src = peaks()
-        avg_pass_ms = pass_ms_max / max(pass_cnt, 1)
-        avg_bytes = pass_bytes / max(pass_cnt, 1)
-        achieved = avg_bytes / (avg_pass_ms / 1e3) / 1e9
-        traffic = None
+        dk = per_kind[dom]
+        achieved = dk["achieved_GBps"]
+        traffic, traffic_src = None, None
         tp = os.path.join(ROOT, "profiles", "pass_kernel_traffic.json")
         if os.path.exists(tp) and not f32 and world == 1:
             try:
-                traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+                tj = json.load(open(tp))
+                traffic = tj.get("per_program", {}).get(dom, {}).get("dram_bytes_per_launch")
+                traffic_src = tj.get("source")
             except Exception:
                 traffic = None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
-            "config": {"workload": f"AQA exact-cover-shaped n={n} (N x 472, seed 0), p={p}, tau=0.4 ns, "
+            "config": {"workload": f"AQA exact-cover-shaped n={n} (N x 472, seed 0), p={p}, tau={TAU} ns, "
                                    f"DW-like schedule; step = |+> + {p} layers + <H_C> + P_success",
                        "n": n, "p": p, "n_local": args.nlocal, "parallelism": f"state sharded over {world} GPU"
                        + ("s (global-qubit swaps)" if world > 1 else ""),
@@ -293,10 +505,14 @@ def main():
                        "l2": f"state {es * (1 << args.nlocal) / 1e9:.1f} GB per GPU >> 126 MB L2 (no flush needed)"},
             "sec_per_layer": ms_step / 1e3 / p,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "qk::tma_pass_kernel", "avg_launch_ms": avg_pass_ms,
-                         "launches": pass_cnt, "alg_bytes_per_launch": avg_bytes,
-                         "pass_share_of_step": pass_ms_max / ms_max},
+                         "frac": achieved / peak, "frac_8TBps": achieved / NORTH_STAR_HBM, "traffic": traffic,
+                         "traffic_source": traffic_src, "peak_source": peak_src,
+                         "kernel": f"qk::tma_pass_kernel ({dom} pass, the largest share of the step)",
+                         "avg_launch_ms": dk["avg_ms"], "launches": dk["launches"],
+                         "alg_bytes_per_launch": dk["alg_bytes_per_launch"],
+                         "pass_share_of_step": pass_ms_max / ms_max,
+                         "per_pass_program": per_kind, "algorithmic_1pass": alg},
+            "extra_configs": extras,
             "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")} if cpu else None),
             "e2e": {"value": (1 << n) * p / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "sec_per_step": e2e_s},
@@ -310,10 +526,10 @@ def main():
                                 "(split swap); implied rate = swap bytes / whole layer time"}
                        if world > 1 else None),
             "clocks": clocks,
-            "results": {"expect_hc": e, "p_success": ps, "r": w["r"]},
+            "results": {"expect_hc": e, "expect_hc_plus_C": e + w["C"], "p_success": ps, "r": w["r"],
+                        "uniform_p": 2.0 ** -n, "tau_ns": TAU},
         }
         print(json.dumps(line), flush=True)
-    sim.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -72,20 +72,30 @@ int qsim_create(int n, int precision, qsim_t **out);
 
 /* Multi-GPU / embedding variant.  The state is partitioned over `world` = 2^g ranks
  * on its top g physical qubits (the "global" qubits): rank r holds the
- * 2^(n-g) amplitudes whose global bits equal r.  `nccl_unique_id` points to the 128
- * bytes of an ncclUniqueId created on rank 0 (qsim_nccl_unique_id) and broadcast to all
- * ranks; an id initialises exactly one communicator, so use a fresh id per handle
- * (ignored when world == 1).  `state_buf` (device pointer, optional) provides caller-owned
- * storage of buf_bytes >= 16 * 2^(n-g) bytes (the library then does not allocate
- * the state); `cuda_stream` (cudaStream_t, optional) is the stream all work is
- * enqueued on.  world must be a power of two <= 8 with n - g >= 13. */
+ * 2^(n-g) amplitudes whose global bits equal r.  `nccl_unique_id` points to 128 bytes
+ * identifying the rank group (ignored when world == 1); a group id initialises exactly one
+ * communicator, so use a fresh id per handle.  Two kinds:
+ *   - an ncclUniqueId from qsim_nccl_unique_id (rank 0 creates it and broadcasts the bytes):
+ *     one process per GPU, NCCL over NVLink, peer buffers mapped with CUDA IPC;
+ *   - a loopback id from qsim_loopback_id (test transport): the `world` ranks are threads of
+ *     ONE process on the current device, each creating its handle with the same id and
+ *     driving it from its own thread (every call is still a collective).  Each rank owns its
+ *     shard buffers and stream; collectives are stream-ordered with CUDA events and a host
+ *     barrier; the pass kernels store into the peers' buffers exactly as over NVLink.
+ * `state_buf` (device pointer, optional) provides caller-owned storage of buf_bytes >= 16 *
+ * 2^(n-g) bytes (the library then does not allocate the state); `cuda_stream` (cudaStream_t,
+ * optional) is the stream all work is enqueued on.  world must be a power of two <= 8 with
+ * n - g >= 15 (QSIM_EUNSUPPORTED otherwise).  Every rank takes the same swap path: the ranks
+ * agree (minimum over ranks) on whether a second shard buffer fits and whether the peer
+ * mappings succeeded. */
 int qsim_create_ex(int n, int precision, int rank, int world, const void *nccl_unique_id,
                    void *state_buf, size_t buf_bytes, void *cuda_stream, qsim_t **out);
 
 int qsim_destroy(qsim_t *q);
 
-/* Upload the Ising problem (eq:HC): h[n] and J[n*n] row-major, of which only the
- * entries with i < j are read.  Values must be finite (QSIM_EINVAL otherwise).
+/* Upload the Ising problem (eq:HC): h[n] and J[n*n] row-major, of which the entries with
+ * i < j are read (the lower triangle is ignored).  Values must be finite and the diagonal
+ * J[i*n + i] zero (QSIM_EINVAL otherwise; eq:HC has no self-coupling).
  * E(z) is bit-exact when every h_i, J_ij is a multiple of 2^-m with
  * sum |coef| 2^m < 2^53 (dyadic data such as the paper's half-integer exact-cover
  * fields); other data is accepted without the bit-exactness claim. */
@@ -127,7 +137,7 @@ int qsim_apply_qsds(qsim_t *q, double tau, int n_steps, const double *s, const d
 
 /* apply `reps` layers of H on every qubit, (H^{otimes n})^reps -- the paper's
  * Hadamard benchmark circuit (H^N)^11 (Table I) -- with the general-mixer tile passes
- * (12 gates per HBM sweep); no phase. */
+ * (12 gates per HBM sweep); no phase, so no qsim_set_ising is needed. */
 int qsim_apply_hadamard(qsim_t *q, int reps);
 
 /* Host-only helper (no device work): the angles qsim_apply_aqa uses. */
@@ -190,6 +200,26 @@ int qsim_plan_positions(int n, int world, int layers, int *pos_out);
  * rank 0, broadcast the bytes, pass them to qsim_create_ex on every rank). */
 int qsim_nccl_unique_id(void *out128);
 
+/* Loopback test transport: write a fresh 128-byte group id for `world` in-process ranks to
+ * out128 (host only; the group is freed when its last handle is destroyed).  QSIM_EINVAL
+ * unless world is 1, 2, 4 or 8. */
+int qsim_loopback_id(int world, void *out128);
+
+/* Which global-qubit swap path the handle runs (collective choice, identical on every rank):
+ *   QSIM_SWAP_NONE            world == 1;
+ *   QSIM_SWAP_FUSED_SPLIT     the passes of a layer store the swapped amplitudes straight into
+ *                             the peers' second buffers (split over the layer's passes);
+ *   QSIM_SWAP_FUSED           the same, all moved by the boundary pass;
+ *   QSIM_SWAP_LOWBIT          fused, low-bit swap schedule (QSIM_LOWSWAP=1, G = 2);
+ *   QSIM_SWAP_COLLECTIVE      out of place through the transport's grouped send/recv;
+ *   QSIM_SWAP_INPLACE_STAGED  in place through a bounded staging ring (no second buffer). */
+enum { QSIM_SWAP_NONE = 0, QSIM_SWAP_FUSED_SPLIT = 1, QSIM_SWAP_FUSED = 2, QSIM_SWAP_LOWBIT = 3,
+       QSIM_SWAP_COLLECTIVE = 4, QSIM_SWAP_INPLACE_STAGED = 5 };
+int qsim_swap_path(const qsim_t *q);
+
+/* Number of qubits of the handle (QSIM_EINVAL for NULL). */
+int qsim_num_qubits(const qsim_t *q);
+
 /* Diagnostics for benchmarking: when enabled, every tile-pass kernel launch is bracketed
  * by CUDA events on the handle's stream.  qsim_profile_read synchronises and returns the
  * summed pass-kernel time (ms), the number of pass launches and their summed algorithmic
@@ -198,9 +228,15 @@ int qsim_nccl_unique_id(void *out128);
 int qsim_profile_enable(qsim_t *q, int on);
 int qsim_profile_read(qsim_t *q, double *ms_sum, uint64_t *count, double *bytes_sum);
 /* Per-pass variant: writes the duration (ms) of each recorded pass, in launch order, into
- * ms_out[0 .. min(count, cap)) and returns the number of recorded passes (>= 0), or a negative
- * error code; clears the record like qsim_profile_read.  Synchronises. */
-int qsim_profile_passes(qsim_t *q, double *ms_out, int cap);
+ * ms_out[0 .. min(count, cap)) and (if kind_out is not NULL) its pass program into kind_out:
+ * bits 0-1 = QSIM_PASS_PLAIN12 / _PLAIN_RUN / _TURN12 / _TURN_RUN (12-bit set or run set, without
+ * or with the cost phase = a "turning" pass), plus the flags QSIM_PASS_MOVING (carries part of a
+ * global-qubit swap), QSIM_PASS_INIT (writes |+> instead of reading), QSIM_PASS_REDUCE (fused
+ * <H_C> / norm).  Returns the number of recorded passes (>= 0) or a negative error code; clears
+ * the record like qsim_profile_read.  Synchronises. */
+enum { QSIM_PASS_PLAIN12 = 0, QSIM_PASS_PLAIN_RUN = 1, QSIM_PASS_TURN12 = 2, QSIM_PASS_TURN_RUN = 3,
+       QSIM_PASS_MOVING = 4, QSIM_PASS_INIT = 8, QSIM_PASS_REDUCE = 16 };
+int qsim_profile_passes(qsim_t *q, double *ms_out, int *kind_out, int cap);
 
 /* Diagnostic micro-benchmark (modifies the state): time `reps` back-to-back launches of
  * the tile pass over tile set `set` (0 = bits 0..11, 1.. = the run sets in ascending bit

@@ -10,8 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libqsim.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("qsim_device.cu", "qsim_tma.cu", "qsim_extra.cu", "qsim_engine.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("qsim_device.h", "qsim_kernels.cuh")] + [
+SOURCES = [os.path.join(CSRC, f) for f in ("qsim_device.cu", "qsim_tma.cu", "qsim_extra.cu", "qsim_comm.cu", "qsim_engine.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("qsim_device.h", "qsim_kernels.cuh", "qsim_comm.h")] + [
     os.path.join(ROOT, "include", "qsim.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -6,11 +6,9 @@
 
 namespace qk {
 
-// dynamic shared memory layout of the pass / reduce kernels
+// dynamic shared memory of the standalone reduction: the launch constants only
 struct SmemLayout {
-    static constexpr size_t tile = SM_TILE_BYTES;  // 64 KiB tile exchange buffer
-    static constexpr size_t cta = ((sizeof(CtaShared) + 15) / 16) * 16;
-    static constexpr size_t total = tile + cta;
+    static constexpr size_t total = ((sizeof(CtaShared) + 15) / 16) * 16;
 };
 static_assert(sizeof(TileRec) == TILE_REC_BYTES, "TileRec size");
 
@@ -113,15 +111,7 @@ __global__ void __launch_bounds__(32 * TF_WARPS) tile_fields_kernel(const PassPa
     }
 }
 
-// ================================================================== tile pass kernel
-// One HBM sweep of the shard, program KIND (PassKind):
-//   PLAIN12:  load X, mix1 X(t7..11) -> Y(t0..4) -> Z(t5,6), [scale], [reduce], store Z
-//   PLAIN_RUN: load X, mix1 X(t7..11) -> W(t3..6), [scale], [reduce], store W
-//   TURN12:   [load X, mix1 X -> Y -> Z | init in Z], phase, mix2 Z -> Y -> X, store X
-//   TURN_RUN: [load X, mix1 X -> W | init in W], phase, mix2 W -> X, store X
-// Grid-stride over tiles with a fixed tile->CTA assignment (deterministic reduction).
-constexpr unsigned MX = 0xF80u, MY = 0x01Fu, MZ = 0x060u, MW = 0x078u;
-
+// ================================================================== L2 prefetch
 // L2 prefetch of tile `ut` (if it exists): its 512 lines of 128 B (tile bits t0..t2 are the
 // low physical bits 0..2 in every set), 4 per thread, so HBM keeps streaming while the CTA
 // computes on the current tile.
@@ -139,105 +129,11 @@ __device__ __forceinline__ void prefetch_next(const PassParams &P, u64 ut, int t
     }
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(NTHR, 2) pass_kernel(const PassParams P) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *sm = reinterpret_cast<double2 *>(smem_raw);
-    CtaShared &cs = *reinterpret_cast<CtaShared *>(smem_raw + SmemLayout::tile);
-    constexpr bool RUN = (KIND == K_PLAIN_RUN || KIND == K_TURN_RUN);
-    constexpr bool TURN = (KIND == K_TURN12 || KIND == K_TURN_RUN);
-    constexpr int FE = RUN ? FW : FZ;  // frame of the phase / reduction
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int n = P.n;
-    const bool need_e = TURN || P.reduce;
-    const TileRec *recs = reinterpret_cast<const TileRec *>(P.rec);
-    int ft = 0;  // tile-bit flips
-#pragma unroll
-    for (int i = 0; i < KT; ++i) ft |= (int)((P.flip >> P.L[i]) & 1ull) << i;
-    const int tE = Frame<FE>::tthr(lane, warp) ^ ft;
-    const int fr = (ft >> Frame<FE>::RB) & 0x1F;
-
-    // launch-constant energy pieces of the phase/reduction frame
-    ThreadEnergy te;
-    double2 pconst = P.scale;
-    double2 u[5];
-    te.eTT = 0.0;
-#pragma unroll
-    for (int r = 0; r < 5; ++r) {
-        te.w[r] = 0.0;
-        u[r] = make_double2(1.0, 0.0);
-    }
-    if (need_e) {
-        te = thread_energy<FE>(P.Jp, n, P.L, lane, warp, ft);
-        if (TURN) {
-            pconst = cmul(P.scale, expmi(P.gamma * te.eTT));
-#pragma unroll
-            for (int r = 0; r < 5; ++r) u[r] = expmi(P.gamma * te.w[r]);
-        }
-        if (tid < NR) {
-            const double e = err_of<FE>(P.Jp, n, P.L, tid ^ fr);
-            cs.eRR[tid] = e;
-            cs.PRR[tid] = TURN ? expmi(P.gamma * e) : make_double2(1.0, 0.0);
-        }
-    }
-    const u64 offX = thread_offset<FX>(P.L, lane, warp);
-    const u64 offS = thread_offset<RUN ? FW : FZ>(P.L, lane, warp);
-
-    double acc_e = 0.0, acc_n = 0.0;
-    double2 v[NR];
-
-    for (u64 ut = blockIdx.x; ut < P.ntiles; ut += gridDim.x) {
-        __syncthreads();  // previous tile done with the smem exchange buffer / launch constants visible
-        const u64 tb = tile_base(P, ut);
-        const TileRec *R = recs + ut;
-        if (!TURN || !P.init) {
-            prefetch_next(P, ut + gridDim.x, tid);
-            load_tile<FX>(v, P.psi + tb + offX, P.L);
-            mix_frame<FX>(v, P.mix1 & MX, P.c1.t);
-            if (RUN) {
-                xch<FX, FW>(v, sm, lane, warp);
-                mix_frame<FW>(v, P.mix1 & MW, P.c1.t);
-            } else {
-                xch<FX, FY>(v, sm, lane, warp);
-                mix_frame<FY>(v, P.mix1 & MY, P.c1.t);
-                xch<FY, FZ>(v, sm, lane, warp);
-                mix_frame<FZ>(v, P.mix1 & MZ, P.c1.t);
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < NR; ++j) v[j] = make_double2(P.a0, 0.0);
-        }
-        if (TURN) {
-            apply_phase<FE>(v, R, tE, fr, pconst, u, cs.PRR);
-            if (RUN) {
-                mix_frame<FW>(v, P.mix2 & MW, P.c2.t);
-                xch<FW, FX>(v, sm, lane, warp);
-            } else {
-                mix_frame<FZ>(v, P.mix2 & MZ, P.c2.t);
-                xch<FZ, FY>(v, sm, lane, warp);
-                mix_frame<FY>(v, P.mix2 & MY, P.c2.t);
-                xch<FY, FX>(v, sm, lane, warp);
-            }
-            mix_frame<FX>(v, P.mix2 & MX, P.c2.t);
-            store_tile<FX>(v, P.psi + tb + offX, P.L);
-        } else {
-            if (P.scale.x != 1.0 || P.scale.y != 0.0) {
-#pragma unroll
-                for (int j = 0; j < NR; ++j) v[j] = cmul(v[j], P.scale);
-            }
-            if (P.reduce) accumulate<FE>(v, R, tE, fr, te, cs.eRR, acc_e, acc_n);
-            store_tile<RUN ? FW : FZ>(v, P.psi + tb + offS, P.L);
-        }
-    }
-    if (P.reduce) block_reduce2(cs, acc_e, acc_n, lane, warp, P.part + 2 * blockIdx.x);
-}
-
 // ============================================================ standalone reduction (frame X)
 template <typename V>
 __global__ void __launch_bounds__(NTHR, 2) reduce_kernel(const PassParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    CtaShared &cs = *reinterpret_cast<CtaShared *>(smem_raw + SmemLayout::tile);
+    CtaShared &cs = *reinterpret_cast<CtaShared *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = P.n;
     const TileRec *recs = reinterpret_cast<const TileRec *>(P.rec);
@@ -294,15 +190,7 @@ __global__ void __launch_bounds__(512) small_kernel(const SmallParams P) {
     __syncthreads();
     for (int k = 0; k < P.p; ++k) {
         const double g = P.ang[k], b = P.ang[P.p + k];
-        for (int z = tid; z < dim; z += nt) {
-            double e = 0.0;
-            for (int i = 0; i < n; ++i) {
-                const double si = ((z >> i) & 1) ? 1.0 : -1.0;
-                e += sh[i] * si;
-                for (int j = i + 1; j < n; ++j) e += sJ[i * n + j] * si * (((z >> j) & 1) ? 1.0 : -1.0);
-            }
-            st[z] = cmul(st[z], expmi(g * e));
-        }
+        for (int z = tid; z < dim; z += nt) st[z] = cmul(st[z], expmi(g * energy_direct(sh, sJ, n, (u64)z)));
         double sb, cb;
         sincos(b, &sb, &cb);
         for (int q = 0; q < n; ++q) {
@@ -336,12 +224,7 @@ __global__ void __launch_bounds__(512) small_kernel(const SmallParams P) {
         psi[z] = av;
         const double2 a = dcast(av);
         if (P.reduce) {
-            double e = 0.0;
-            for (int i = 0; i < n; ++i) {
-                const double si = ((z >> i) & 1) ? 1.0 : -1.0;
-                e += sh[i] * si;
-                for (int j = i + 1; j < n; ++j) e += sJ[i * n + j] * si * (((z >> j) & 1) ? 1.0 : -1.0);
-            }
+            const double e = energy_direct(sh, sJ, n, (u64)z);
             const double pz = fma(a.x, a.x, a.y * a.y);
             acc_e = fma(pz, e, acc_e);
             acc_n += pz;
@@ -394,27 +277,57 @@ __global__ void gather_kernel(const GatherParams G, const V *psi, double2 *out) 
     }
 }
 
-__global__ void energy_probe_kernel(const GatherParams G, const double *hp, const double *Jp,
-                                    const ProbeSet S, double *out) {
+// E(z) of the labels [first, first + count) with the hot path's own arithmetic (qsim_energies):
+// m > 12: the record of the label's tile of set S (written by tile_fields_kernel, flip 0) and the
+// thread / register decomposition of frame Z, summed exactly as accumulate<FZ> sums the reducing
+// pass's energies (base, then the register-bit chain r = 0..4, then E_RR); m <= 12: the direct
+// sum of small_kernel.  Multi-GPU: the rank owning the label's physical index writes E, the
+// others 0 (the engine sums over ranks).
+__global__ void energy_dump_kernel(const GatherParams G, const PassParams P, double *out) {
+    const TileRec *recs = reinterpret_cast<const TileRec *>(P.rec);
     for (u64 k = blockIdx.x * (u64)blockDim.x + threadIdx.x; k < G.count; k += (u64)gridDim.x * blockDim.x) {
         const u64 x = logical_to_physical(G.first + k, G);
-        out[k] = energy_point(hp, Jp, G.n, S.L, S.k, S.lmask, x);
+        if ((x >> G.m) != G.rank) {
+            out[k] = 0.0;
+            continue;
+        }
+        if (G.m <= KT) {
+            out[k] = energy_direct(P.hp, P.Jp, G.n, x);
+            continue;
+        }
+        const u64 xl = x & ((1ull << G.m) - 1ull);
+        u64 u = 0;  // tile id: the non-tile bits in ascending order (inverse of tile_base)
+        int src = 0;
+        for (int sg = 0; sg < P.nseg; ++sg) {
+            u |= ((xl >> P.seg_dst[sg]) & ((1ull << P.seg_len[sg]) - 1ull)) << src;
+            src += P.seg_len[sg];
+        }
+        int t = 0;
+#pragma unroll
+        for (int i = 0; i < KT; ++i) t |= (int)((xl >> P.L[i]) & 1ull) << i;
+        constexpr int RB = Frame<FZ>::RB;
+        const int tthr = t & ~(0x1F << RB), j = (t >> RB) & 0x1F;
+        const ThreadEnergy te = thread_energy<FZ>(P.Jp, G.n, P.L, tthr & 31, tthr >> 10, 0);
+        const TileRec &R = recs[u];
+        double e = R.e[KT] + te.eTT;
+#pragma unroll
+        for (int i = 0; i < KT; ++i) {
+            if (i >= RB && i < RB + 5) continue;
+            e += ((tthr >> i) & 1) ? R.e[i] : -R.e[i];
+        }
+#pragma unroll
+        for (int r = 0; r < 5; ++r) {
+            const double a = R.e[RB + r] + te.w[r];
+            e = ((j >> r) & 1) ? e + a : e - a;
+        }
+        out[k] = e + err_of<FZ>(P.Jp, G.n, P.L, j);
     }
 }
 
 // ======================================================================== launchers
-size_t pass_smem_bytes() { return SmemLayout::total; }
 
 cudaError_t setup_kernels() {
     cudaError_t e;
-    e = cudaFuncSetAttribute(pass_kernel<K_PLAIN12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmemLayout::total);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(pass_kernel<K_PLAIN_RUN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmemLayout::total);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(pass_kernel<K_TURN12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmemLayout::total);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(pass_kernel<K_TURN_RUN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmemLayout::total);
-    if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(reduce_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)SmemLayout::total);
     if (e != cudaSuccess) return e;
@@ -424,17 +337,6 @@ cudaError_t setup_kernels() {
     e = cudaFuncSetAttribute(small_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * TILE);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(small_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * TILE);
-}
-
-cudaError_t launch_pass(const PassParams &P, int grid, cudaStream_t s) {
-    switch (P.kind) {
-        case K_PLAIN12: pass_kernel<K_PLAIN12><<<grid, NTHR, SmemLayout::total, s>>>(P); break;
-        case K_PLAIN_RUN: pass_kernel<K_PLAIN_RUN><<<grid, NTHR, SmemLayout::total, s>>>(P); break;
-        case K_TURN12: pass_kernel<K_TURN12><<<grid, NTHR, SmemLayout::total, s>>>(P); break;
-        case K_TURN_RUN: pass_kernel<K_TURN_RUN><<<grid, NTHR, SmemLayout::total, s>>>(P); break;
-        default: return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
 }
 
 cudaError_t launch_tile_fields(const PassParams &P, void *rec, cudaStream_t s) {
@@ -472,9 +374,8 @@ cudaError_t launch_gather(const GatherParams &G, const double2 *psi, double2 *ou
     return cudaGetLastError();
 }
 
-cudaError_t launch_energy_probe(const GatherParams &G, const double *hp, const double *Jp, const ProbeSet &S,
-                                double *out, int grid, cudaStream_t s) {
-    energy_probe_kernel<<<grid, 256, 0, s>>>(G, hp, Jp, S, out);
+cudaError_t launch_energy_dump(const GatherParams &G, const PassParams &P, double *out, int grid, cudaStream_t s) {
+    energy_dump_kernel<<<grid, 256, 0, s>>>(G, P, out);
     return cudaGetLastError();
 }
 

@@ -79,28 +79,16 @@ struct PassParams {
     // so that the tiles in flight at one time span all groups (moving passes interleave NVLink
     // and HBM traffic instead of alternating phases of each); 0 = natural order
     int ord_rot, ord_bits;
-    // CTA tile assignment: groups of 2^ord_grp address-adjacent tiles (tile-id bit 0 = physical
-    // bit 3 of a run set) go to one CTA back to back, so the two groups load and store
-    // neighbouring 128-byte rows together; 0 = cyclic (tile k to CTA k mod grid)
-    int ord_grp;
-    int defer;           // turning-run passes: refill a TMA-stored stage one tile later (no store wait)
     // e^{-i gamma E_RR(j ^ fr)} of the turning-run phase frame's 32 register patterns, computed on
     // the host (FP64 R_x turning-run passes of the single-GPU and top-bit schedules): read from
     // the constant bank instead of shared memory
     double2 PRR[NR];
     int dbg;             // diagnostics (qsim_bench_pass): bit 0 skip stores, bit 1 skip state loads
     int tma_store;       // store tiles with TMA from the stage instead of STG from registers
-    int l2hint;          // L2 cache policy: bits 0-1 loads, bits 2-3 stores (0 none, 1 evict_first, 2 evict_last)
-    // out-of-place tile-major store (single-GPU relabelling schedule): tile u goes to the
-    // contiguous block out + (out_u << 12), out_u = sum_s ((u >> src_s) & (2^len_s - 1)) << dst_s
     // general mixer (QSDS combined step, NEXT-1): per tile bit a 2x2 complex matrix
     // {m00, m01, m10, m11} acting on (|0>, |1>) instead of the scaled R_x butterfly
     int gmix;
     double2 gm1[KT][4], gm2[KT][4];
-    int tmo;
-    double2 *out;
-    int onseg;
-    int oseg_src[20], oseg_len[20], oseg_dst[20];
 };
 
 constexpr size_t TILE_REC_BYTES = 320;  // sizeof(TileRec)
@@ -131,23 +119,18 @@ struct EnumParams {
     u64 u0, u1;              // tile range (tile u = labels u*4096 .. u*4096+4095)
     int collect;             // 0: per-CTA minimum into part; 1: collect labels with E == emin
     double emin;
-    u64 *out;
-    unsigned long long *count;
+    u64 *out;                // collect: per CTA max_out slots (out + blockIdx.x * max_out), ascending
+    unsigned *cta_cnt;       // collect: labels written per CTA
+    unsigned long long *count;  // collect: += number of minimisers
     int max_out;
     double *part;
 };
 
-struct ProbeSet {
-    int L[KT];
-    int k;
-    u64 lmask;
-};
 
 cudaError_t launch_spin(const PassParams &P, double *part, int grid, cudaStream_t s);
 cudaError_t launch_sum_vec(const double *part, int nparts, int n, double *out, cudaStream_t s);
 cudaError_t launch_enum(const EnumParams &E, int grid, cudaStream_t s);
 cudaError_t launch_min_partials(const double *part, int nparts, double *res, cudaStream_t s);
-size_t pass_smem_bytes();
 size_t tma_smem_bytes();
 cudaError_t setup_tma_kernels();
 // TMA-pipelined pass (qsim_tma.cu); `tensor_map` points to a CUtensorMap (128 B)
@@ -155,7 +138,6 @@ cudaError_t setup_tma_kernels();
 cudaError_t launch_tma_pass(const ::CUtensorMap_st &tensor_map, const ::CUtensorMap_st &store_map,
                             const PassParams &P, int grid, cudaStream_t s);
 cudaError_t setup_kernels();
-cudaError_t launch_pass(const PassParams &P, int grid, cudaStream_t s);
 cudaError_t launch_tile_fields(const PassParams &P, void *rec, cudaStream_t s);
 cudaError_t launch_reduce(const PassParams &P, int grid, cudaStream_t s);
 cudaError_t launch_sum_partials(const double *part, int nparts, double *res, cudaStream_t s);
@@ -163,7 +145,6 @@ cudaError_t launch_small(const SmallParams &P, cudaStream_t s);
 cudaError_t launch_init_plus(double2 *psi, u64 count, double a0, int grid, cudaStream_t s, int f32 = 0);
 cudaError_t launch_gather(const GatherParams &G, const double2 *psi, double2 *out, int grid, cudaStream_t s,
                           int f32 = 0);
-cudaError_t launch_energy_probe(const GatherParams &G, const double *hp, const double *Jp,
-                                const ProbeSet &S, double *out, int grid, cudaStream_t s);
+cudaError_t launch_energy_dump(const GatherParams &G, const PassParams &P, double *out, int grid, cudaStream_t s);
 
 }  // namespace qk

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/qsim.h"
+#include "qsim_comm.h"
 #include "qsim_device.h"
 
 using qk::u64;
@@ -340,16 +341,15 @@ struct qsim {
     // set's pass (PassParams::wsh)
     bool lowswap = false;
     bool ls_now = false;  // the current apply_layers call runs the low-bit swap schedule (R_x mixers)
-    double ls_share = 0.5;  // share of the swap moved by the turning pass (QSIM_LS_SHARE)
+    double ls_share = 0.5;  // share of the swap moved by the turning pass
     int mv_pshift = 0, mv_pbits = 0;
     std::vector<double> split_w;
     int cur = 0;                       // which of bufs[] currently holds the state
     double2 *bufs[2] = {nullptr, nullptr};
     double2 *peer[2][8] = {};          // peer[b][c] = rank c's buffer b (own buffer for c == rank)
-    double *d_bar = nullptr;           // 1-double scratch for the NCCL barrier
     cudaStream_t st = nullptr;
     bool own_stream = false;
-    ncclComm_t comm = nullptr;
+    qc::Comm *comm = nullptr;          // cross-rank transport (NCCL + CUDA IPC, or the loopback)
     bool has_ising = false;
     std::vector<double> h, J;  // logical, J symmetric with zero diagonal
     int pos[qk::NMAX];         // logical qubit -> physical bit position (the paper's permutation array)
@@ -367,8 +367,6 @@ struct qsim {
     bool hmode = false;        // Hadamard layers (gmats holds H): dedicated butterfly
     bool frame_noh = false;
     bool fr_noh_built = false;
-    bool tilemajor = false;    // single GPU: out-of-place relabelling schedule (second buffer)
-    TileSet tmset;             // its fixed tile shape: bits {0,1,2} + {12..20}
     double *d_part = nullptr, *d_res = nullptr, *d_ang = nullptr;
     size_t ang_cap = 0;
     void *d_scratch = nullptr;
@@ -378,19 +376,14 @@ struct qsim {
     bool pending_plus = true;
     bool res_valid = false;
     uint64_t launches = 0;
-    int prefetch = 1;          // L2 prefetch of the next tile (QSIM_PREFETCH=0 disables, for experiments)
-    int use_tma = 1;           // TMA-pipelined pass kernel (QSIM_KERNEL=v4 selects the register-direct one)
-    int l2promo = (int)CU_TENSOR_MAP_L2_PROMOTION_L2_128B;  // TMA L2 sector promotion (QSIM_L2PROMO=0..3)
     int tma_store = 1;         // TMA stores from the stage (QSIM_TMA_STORE=0: STG from registers)
-    int l2hint = 0;            // TMA L2 cache policy (QSIM_L2HINT, see PassParams::l2hint)
-    int ord_grp = 0;           // adjacent-tile groups per CTA for run sets (QSIM_ORD_GRP, PassParams::ord_grp)
-    int defer = 1;             // deferred stage refill after TMA stores (QSIM_DEFER, PassParams::defer)
     std::string err;
     // optional per-pass timing (CUDA events on the handle's stream around each pass launch)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     std::vector<double> prof_bytes;  // algorithmic bytes of each recorded pass
+    std::vector<int> prof_kind;      // its pass program (qsim_profile_passes)
 };
 
 namespace {
@@ -408,11 +401,9 @@ int fail(qsim *q, int code, const std::string &msg) {
             return fail(q, QSIM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
     } while (0)
 
-#define NK(call)                                                                              \
+#define CM(call)                                                                              \
     do {                                                                                      \
-        ncclResult_t r_ = (call);                                                             \
-        if (r_ != ncclSuccess)                                                                \
-            return fail(q, QSIM_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));   \
+        if (!(call)) return fail(q, QSIM_ENCCL, std::string(#call) + ": " + q->comm->error()); \
     } while (0)
 
 int grid_for(const qsim *q, u64 ntiles) {
@@ -525,13 +516,10 @@ qk::PassParams base_params(qsim *q, const TileSet &S) {
     P.a0 = std::pow(2.0, -0.5 * q->n);
     P.part = q->d_part;
     P.scale = make_double2(1.0, 0.0);
-    // L2 prefetch pays only for the contiguous 64 KiB tiles of the 12-bit set; for run sets
-    // every tile touches up to 512 distinct 2 MiB pages and prefetching slows them (measured)
-    P.prefetch = q->prefetch && S.full12;
+    // L2 prefetch (standalone reduction) pays only for the contiguous 64 KiB tiles of the 12-bit
+    // set; for run sets every tile touches up to 512 distinct 2 MiB pages (measured slower)
+    P.prefetch = S.full12;
     P.tma_store = q->tma_store;
-    P.l2hint = q->l2hint;
-    P.ord_grp = S.full12 ? 0 : std::min(q->ord_grp, (int)(q->m - qk::KT));
-    P.defer = q->defer;
     return P;
 }
 
@@ -547,9 +535,9 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     return fn;
 }
 
-// launch one pass: TMA-pipelined kernel (one CTA per SM) or the register-direct kernel
+// launch one pass: TMA-pipelined kernel (one CTA per SM)
 // `out`: output buffer of an out-of-place pass (TMA stores go there), nullptr = in place
-int launch_pass_any(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, double2 *out = nullptr) {
+int launch_pass(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, double2 *out = nullptr) {
     if (P.kind == qk::K_TURN_RUN && P.gmix == 0 && !P.f32 && P.multi != 2) {
         // pattern factors of the phase frame (W: register bits = tile bits 3..7), the same sums
         // as err_of<FW> over the current physical frame of J
@@ -567,7 +555,7 @@ int launch_pass_any(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out,
             P.PRR[j] = make_double2(std::cos(th), -std::sin(th));
         }
     }
-    if (q->use_tma) {
+    {
         auto enc = tmap_encoder();
         if (!enc) return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled unavailable");
         CUtensorMap tm[2];
@@ -576,7 +564,7 @@ int launch_pass_any(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out,
         for (int k = 0; k < (out ? 2 : 1); ++k) {
             CUresult r = enc(&tm[k], dt, 5u, (void *)(k ? out : q->psi), S.tm_dim,
                              S.tm_stride + 1, S.tm_box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                             (CUtensorMapL2promotion)q->l2promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS)
                 return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
         }
@@ -587,10 +575,6 @@ int launch_pass_any(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out,
         int grid = (int)std::min<u64>((u64)q->num_sms, S.ntiles);
         CK(qk::launch_tma_pass(tm[0], out ? tm[1] : tm[0], P, grid, q->st));
         *grid_out = grid;
-    } else {
-        int grid = grid_for(q, S.ntiles);
-        CK(qk::launch_pass(P, grid, q->st));
-        *grid_out = grid;
     }
     q->launches++;
     return QSIM_OK;
@@ -599,7 +583,7 @@ int launch_pass_any(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out,
 int finish_reduce(qsim *q, int nparts) {
     CK(qk::launch_sum_partials(q->d_part, nparts, q->d_res, q->st));
     q->launches++;
-    if (q->world > 1) NK(ncclAllReduce(q->d_res, q->d_res, 2, ncclDouble, ncclSum, q->comm, q->st));
+    if (q->world > 1) CM(q->comm->allreduce(q->d_res, 2, qc::Op::Sum, q->st));
     q->res_valid = true;
     return QSIM_OK;
 }
@@ -616,7 +600,7 @@ void swap_bookkeeping(qsim *q) {
 // is done, then the other buffer holds the state; after the layer's last moving pass the
 // relabelling takes effect
 int finish_fused_swap(qsim *q, bool done) {
-    NK(ncclAllReduce(q->d_bar, q->d_bar, 1, ncclDouble, ncclSum, q->comm, q->st));
+    CM(q->comm->barrier(q->st));
     q->cur ^= 1;
     q->psi = q->bufs[q->cur];
     q->tmp = q->bufs[q->cur ^ 1];
@@ -630,16 +614,12 @@ int do_swap(qsim *q) {
     swap_bookkeeping(q);
     const u64 chunk = 1ull << (q->m - q->g);  // amplitudes per chunk
     const size_t cbytes = chunk * q->es;
-    const size_t cdbl = cbytes / 8;           // chunk in doubles (NCCL count)
     auto at = [&](double2 *b, u64 amp) { return (double2 *)((char *)b + amp * q->es); };
     if (q->tmp) {
-        NK(ncclGroupStart());
-        for (int c = 0; c < G; ++c) {
-            if (c == q->rank) continue;
-            NK(ncclSend(at(q->psi, c * chunk), cdbl, ncclDouble, c, q->comm, q->st));
-            NK(ncclRecv(at(q->tmp, c * chunk), cdbl, ncclDouble, c, q->comm, q->st));
-        }
-        NK(ncclGroupEnd());
+        std::vector<qc::XPair> xs;
+        for (int c = 0; c < G; ++c)
+            if (c != q->rank) xs.push_back({c, at(q->psi, c * chunk), at(q->tmp, c * chunk), cbytes});
+        CM(q->comm->exchange(xs, q->st));
         CK(cudaMemcpyAsync(at(q->tmp, q->rank * chunk), at(q->psi, q->rank * chunk), cbytes,
                            cudaMemcpyDeviceToDevice, q->st));
         std::swap(q->psi, q->tmp);
@@ -652,22 +632,16 @@ int do_swap(qsim *q) {
         if (rc) return rc;
         double2 *stg = (double2 *)q->d_scratch;
         for (u64 off = 0; off < chunk; off += piece) {
+            std::vector<qc::XPair> xs;
             int slot = 0;
             for (int c = 0; c < G; ++c) {
                 if (c == q->rank) continue;
                 CK(cudaMemcpyAsync(at(stg, (u64)slot * piece), at(q->psi, c * chunk + off), piece * q->es,
                                    cudaMemcpyDeviceToDevice, q->st));
+                xs.push_back({c, at(stg, (u64)slot * piece), at(q->psi, c * chunk + off), piece * q->es});
                 ++slot;
             }
-            NK(ncclGroupStart());
-            slot = 0;
-            for (int c = 0; c < G; ++c) {
-                if (c == q->rank) continue;
-                NK(ncclSend(at(stg, (u64)slot * piece), piece * q->es / 8, ncclDouble, c, q->comm, q->st));
-                NK(ncclRecv(at(q->psi, c * chunk + off), piece * q->es / 8, ncclDouble, c, q->comm, q->st));
-                ++slot;
-            }
-            NK(ncclGroupEnd());
+            CM(q->comm->exchange(xs, q->st));
         }
     }
     return QSIM_OK;
@@ -713,15 +687,12 @@ void set_gmix(const qsim *q, qk::PassParams &P, const int *L, const PassOp &op) 
     }
 }
 
-int apply_tilemajor(qsim *q, const double *gam, const double *bet, int p);
-
 int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
     if (q->pending_plus) reset_perm(q);  // the first pass writes |+>^n: any labelling is valid
     {
         int rc = ensure_frame(q);
         if (rc) return rc;
     }
-    if (q->tilemajor) return apply_tilemajor(q, gam, bet, p);
     if (q->m <= qk::KT) {  // whole state in one CTA (single GPU only)
         if ((size_t)2 * p > q->ang_cap) {
             if (q->d_ang) cudaFree(q->d_ang);
@@ -795,9 +766,9 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
     int last_grid = 0;
     // the scaled butterflies' pass-wide scalars kappa^m are global factors: the plain passes'
     // ones ride on the next phase (turning) or reducing pass, which multiplies anyway, so the
-    // plain passes do no per-amplitude scaling (QSIM_CARRY=0 restores per-pass scaling)
+    // plain passes do no per-amplitude scaling
     std::complex<double> carry(1.0, 0.0);
-    const bool carry_on = !q->gmats && !(std::getenv("QSIM_CARRY") && std::atoi(std::getenv("QSIM_CARRY")) == 0);
+    const bool carry_on = !q->gmats;
     for (const PassOp &op : ops) {
         const TileSet &S = q->sets[op.set];
         {
@@ -888,13 +859,15 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
             CK(cudaEventRecord(e0, q->st));
         }
         {
-            int rc = launch_pass_any(q, S, P, &grid, outbuf);
+            int rc = launch_pass(q, S, P, &grid, outbuf);
             if (rc) return rc;
         }
         if (q->prof) {
             CK(cudaEventRecord(e1, q->st));
             // algorithmic HBM bytes: read + write of the shard, write only for the init pass
             q->prof_bytes.push_back((op.init ? 1.0 : 2.0) * (double)q->es * (double)(1ull << q->m));
+            q->prof_kind.push_back(P.kind | (op.mv ? QSIM_PASS_MOVING : 0) | (op.init ? QSIM_PASS_INIT : 0) |
+                                   (op.reduce ? QSIM_PASS_REDUCE : 0));
         }
         last_grid = grid;
         if (op.mv) {
@@ -905,152 +878,6 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
             int rc = do_swap(q);
             if (rc) return rc;
         }
-    }
-    q->pending_plus = false;
-    q->ls_now = false;
-    if (q->gmats) return QSIM_OK;  // J-only frame: <H_C> is recomputed on demand
-    return finish_reduce(q, last_grid);
-}
-
-// Single-GPU relabelling schedule (m >= 21, needs a second state buffer).  Every
-// pass reads tiles of the fixed shape L = {0,1,2} + {12..20} (TMA: 128-byte rows at a 64 KiB
-// stride, 16 pages per tile) and writes each tile as one contiguous 64 KiB block of the other
-// buffer.  Writing the tile bits to positions 0..11 and the tile-id bits in a chosen order is a
-// qubit relabelling; it is chosen so that the next pass's qubits sit at positions 12.. .  Groups
-// (from the layout at entry): 0 = the qubits at 0..11 (mixed together, all 12 tile bits), 1..K =
-// the runs over 12..m-1 (<= 9 each, balanced).  Passes follow the same boustrophedon as
-// build_schedule ((K) p + 1 passes); a run shorter than 9 fills its tile with "filler" qubits
-// of a run that is neither this pass's nor the next pass's.
-int apply_tilemajor(qsim *q, const double *gam, const double *bet, int p) {
-    const int n = q->n, m = q->m;
-    const TileSet &S = q->tmset;
-    const int R = m - qk::KT;
-    const int K = (R + 8) / 9;
-    std::vector<int> gid(n, -1);
-    for (int x = 0; x < qk::KT; ++x) gid[q->qat[x]] = 0;
-    {
-        int x = qk::KT;
-        for (int k = 1; k <= K; ++k) {
-            const int len = R / K + (k <= R % K ? 1 : 0);
-            for (int i = 0; i < len; ++i) gid[q->qat[x++]] = k;
-        }
-    }
-    std::vector<PassOp> ops = build_schedule(K + 1, 0, p, gam, bet, q->pending_plus, false);
-    bool tile_pos[qk::NMAX] = {};
-    for (int t = 0; t < qk::KT; ++t) tile_pos[S.L[t]] = true;
-    int last_grid = 0;
-    for (size_t i = 0; i < ops.size(); ++i) {
-        const PassOp &op = ops[i];
-        const int gi = op.set;
-        const int gn = i + 1 < ops.size() ? ops[i + 1].set : -1;
-        const int gnn = i + 2 < ops.size() ? ops[i + 2].set : -1;
-        int rc = ensure_frame(q);
-        if (rc) return rc;
-        // tile bits of this pass that hold its group's qubits
-        unsigned own = 0;
-        for (int t = 0; t < qk::KT; ++t)
-            if (gid[q->qat[S.L[t]]] == gi) own |= 1u << t;
-        if (gi > 0)  // a run: its qubits must be at the top-of-tile positions 12..
-            for (int t = 0; t < 3; ++t)
-                if ((own >> t) & 1u) return fail(q, QSIM_ECUDA, "relabel plan: run qubit at a passenger position");
-        // ---- output labelling: tile bit t -> position t; tile-id qubits -> 12.. with the next
-        // group first, then its fillers, then the rest in ascending position
-        int newp[qk::NMAX];
-        for (int t = 0; t < qk::KT; ++t) newp[S.L[t]] = t;
-        std::vector<int> ids;  // non-tile positions ascending (= tile-id bit order)
-        for (int x = 0; x < m; ++x)
-            if (!tile_pos[x]) ids.push_back(x);
-        std::vector<bool> placed(m, false);
-        int nextp = qk::KT;
-        if (gn >= 0) {
-            for (int x : ids)
-                if (gid[q->qat[x]] == gn) {
-                    newp[x] = nextp++;
-                    placed[x] = true;
-                }
-            const int need = gn > 0 ? qk::KT + 9 - nextp : 0;
-            int got = 0;
-            for (int x : ids) {
-                if (got >= need) break;
-                const int gx = gid[q->qat[x]];
-                if (placed[x] || gx == 0 || gx == gn || gx == gnn) continue;
-                newp[x] = nextp++;
-                placed[x] = true;
-                ++got;
-            }
-            if (got < need) return fail(q, QSIM_ECUDA, "relabel plan: not enough filler qubits");
-            // the next group must be entirely in this pass's tile-id bits
-            for (int t = 0; t < qk::KT; ++t)
-                if (gn > 0 && gid[q->qat[S.L[t]]] == gn) return fail(q, QSIM_ECUDA, "relabel plan: next group in tile");
-            for (int t = 3; t < qk::KT; ++t)
-                if (gn == 0 && gid[q->qat[S.L[t]]] == 0 && S.L[t] >= qk::KT)
-                    return fail(q, QSIM_ECUDA, "relabel plan: next group in tile");
-        }
-        for (int x : ids)
-            if (!placed[x]) newp[x] = nextp++;
-        // output tile id segments: tile-id bit k (position ids[k]) -> bit newp[ids[k]] - 12
-        qk::PassParams P = base_params(q, S);
-        P.onseg = 0;
-        for (size_t k = 0; k < ids.size();) {
-            size_t e = k + 1;
-            while (e < ids.size() && newp[ids[e]] == newp[ids[e - 1]] + 1) ++e;
-            if (P.onseg == 20) return fail(q, QSIM_ECUDA, "relabel plan: too many segments");
-            P.oseg_src[P.onseg] = (int)k;
-            P.oseg_len[P.onseg] = (int)(e - k);
-            P.oseg_dst[P.onseg] = newp[ids[k]] - qk::KT;
-            ++P.onseg;
-            k = e;
-        }
-        P.tmo = 1;
-        P.out = q->bufs[q->cur ^ 1];
-        P.prefetch = 0;
-        // ---- mixing, phase, flips (as in the in-place schedule)
-        std::complex<double> k1(1.0, 0.0), k2(1.0, 0.0);
-        P.c1 = mix_coef(op.b1, k1);
-        P.c2 = mix_coef(op.b2, k2);
-        P.mix1 = op.mix1 & own;
-        P.mix2 = op.phase ? (op.mix2 & own) : 0u;
-        std::complex<double> sc = cpow_int(k1, __builtin_popcount(P.mix1)) * cpow_int(k2, __builtin_popcount(P.mix2));
-        P.scale = make_double2(sc.real(), sc.imag());
-        set_gmix(q, P, S.L, op);
-        auto posmask = [&](unsigned tm) {
-            u64 r = 0;
-            for (int t = 0; t < qk::KT; ++t)
-                if ((tm >> t) & 1u) r |= 1ull << S.L[t];
-            return r;
-        };
-        const u64 f1 = P.c1.form ? posmask(P.mix1) : 0ull;
-        const u64 f2 = P.c2.form ? posmask(P.mix2) : 0ull;
-        P.flip = q->flip ^ f1;
-        q->flip = P.flip ^ f2;
-        P.kind = gi == 0 ? (op.phase ? qk::K_TURN12 : qk::K_PLAIN12) : (op.phase ? qk::K_TURN_RUN : qk::K_PLAIN_RUN);
-        P.init = op.init;
-        P.phase = op.phase;
-        P.reduce = op.reduce;
-        P.gamma = op.gamma;
-        P.rec = q->d_rec;
-        if (op.phase || op.reduce) {
-            CK(qk::launch_tile_fields(P, q->d_rec, q->st));
-            q->launches++;
-        }
-        int grid = 0;
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (q->prof) {
-            rc = prof_events(q, &e0, &e1);
-            if (rc) return rc;
-            CK(cudaEventRecord(e0, q->st));
-        }
-        rc = launch_pass_any(q, S, P, &grid);
-        if (rc) return rc;
-        if (q->prof) {
-            CK(cudaEventRecord(e1, q->st));
-            q->prof_bytes.push_back((op.init ? 16.0 : 32.0) * (double)(1ull << m));
-        }
-        last_grid = grid;
-        relabel(q, newp);
-        q->cur ^= 1;
-        q->psi = q->bufs[q->cur];
-        q->tmp = q->bufs[q->cur ^ 1];
     }
     q->pending_plus = false;
     q->ls_now = false;
@@ -1087,7 +914,7 @@ int run_reduce(qsim *q) {
         q->res_valid = true;
         return QSIM_OK;
     }
-    const TileSet &S = q->tilemajor ? q->tmset : q->sets[0];
+    const TileSet &S = q->sets[0];
     qk::PassParams P = base_params(q, S);
     P.rec = q->d_rec;
     P.flip = q->flip;
@@ -1131,7 +958,7 @@ int gather_host(qsim *q, u64 first, u64 count, const uint64_t *hlist, double *ou
         qk::GatherParams G = gather_params(q, first + done, c, dlist);
         CK(qk::launch_gather(G, q->psi, dout, (int)std::min<u64>((c + 255) / 256, 4096), q->st, q->f32));
         q->launches++;
-        if (q->world > 1) NK(ncclAllReduce(dout, dout, c * 2, ncclDouble, ncclSum, q->comm, q->st));
+        if (q->world > 1) CM(q->comm->allreduce((double *)dout, c * 2, qc::Op::Sum, q->st));
         CK(cudaMemcpyAsync(out + 2 * done, dout, c * sizeof(double2), cudaMemcpyDeviceToHost, q->st));
         CK(cudaStreamSynchronize(q->st));
     }
@@ -1182,11 +1009,7 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     CK(cudaMalloc(&q->d_part, sizeof(double) * 2 * 4 * q->num_sms));
     CK(cudaMalloc(&q->d_res, sizeof(double) * 2));
     if (q->m > qk::KT) {
-        int minpass = 3;
-        if (const char *e = std::getenv("QSIM_F32_PASSENGERS"); q->f32 && e) minpass = std::max(3, std::min(6, std::atoi(e)));
-        if (const char *e = std::getenv("QSIM_PASSENGERS")) minpass = std::max(3, std::min(6, std::atoi(e)));
-        const char *bal = std::getenv("QSIM_RUNS_BALANCED");
-        q->sets = build_sets(q->m, (int)q->es, minpass, !(bal && std::atoi(bal) == 0));
+        q->sets = build_sets(q->m, (int)q->es);
         // Split runs (one GPU, two 9-bit runs, i.e. m = 30): run 1 takes the bits [12, 12+a) and
         // the top 9-a bits, run 2 the 9 bits between.  With 128-byte rows a run on the top
         // bits [21, 30) streams at 61-69 % of HBM even for reads alone (the run on [12, 21) at
@@ -1210,38 +1033,15 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
         }
         CK(cudaMalloc(&q->d_rec, qk::TILE_REC_BYTES << (q->m - qk::KT)));
     }
-    if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
-    if (world == 1 && q->m >= qk::KT + 9 && q->use_tma && !buf && !q->f32) {
-        // relabelling schedule: needs a second buffer (kept only if >= 8 GiB stay free)
-        // (measured slower than the in-place schedule on B200: concurrent scattered reads and
-        // contiguous writes stream at ~84 % while either alone runs at ~98 %; opt-in only)
-        const char *tz = std::getenv("QSIM_TILEMAJOR");
-        size_t fr = 0, tot = 0;
-        CK(cudaMemGetInfo(&fr, &tot));
-        if (tz && std::atoi(tz) == 1 && fr > bytes + (8ull << 30)) {
-            if (cudaMalloc(&q->tmp, bytes) == cudaSuccess) {
-                std::vector<int> L;
-                for (int i = 0; i < 3; ++i) L.push_back(i);
-                for (int i = qk::KT; i < qk::KT + 9; ++i) L.push_back(i);
-                q->tmset = make_set(q->m, L, (1u << qk::KT) - 1);
-                q->tmset.full12 = false;
-                q->bufs[0] = q->psi;
-                q->bufs[1] = q->tmp;
-                q->cur = 0;
-                q->tilemajor = q->tmset.tm_ok;
-            } else {
-                cudaGetLastError();
-                q->tmp = nullptr;
-            }
-        }
-    }
     if (world > 1) {
-        ncclUniqueId id;
-        std::memcpy(&id, uid, sizeof(id));
-        NK(ncclCommInitRank(&q->comm, world, id, rank));
-        if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
-        // out-of-place swap buffer when it leaves >= 8 GiB free, else in-place staging
-        // (QSIM_SWAP_INPLACE=1 forces the in-place path, for tests)
+        {
+            std::string cerr;
+            q->comm = qc::make_comm(uid, world, rank, &cerr);
+            if (!q->comm) return fail(q, QSIM_ENCCL, "communicator: " + cerr);
+        }
+        // out-of-place swap buffer when it leaves >= 8 GiB free on EVERY rank, else in-place
+        // staging (QSIM_SWAP_INPLACE=1 forces the in-place path, for tests).  The ranks agree
+        // before branching: the schedules differ in their collectives.
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot));
         const char *ip = std::getenv("QSIM_SWAP_INPLACE");
@@ -1251,36 +1051,29 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
                 q->tmp = nullptr;
             }
         }
-        CK(cudaMalloc(&q->d_bar, sizeof(double)));
-        CK(cudaMemsetAsync(q->d_bar, 0, sizeof(double), q->st));
-        // fused swap: map every rank's two state buffers (CUDA IPC handles all-gathered over NCCL)
+        long long all_tmp = 0;
+        CM(q->comm->agree_min(q->tmp ? 1 : 0, &all_tmp, q->st));
+        if (!all_tmp && q->tmp) {
+            cudaFree(q->tmp);
+            q->tmp = nullptr;
+        }
+        // fused swap: map every rank's two state buffers (CUDA IPC, or the loopback's pointers);
+        // if any rank cannot map, all keep the separate swap
         const char *fz = std::getenv("QSIM_FUSED_SWAP");
-        if (q->tmp && !q->user_buf && q->use_tma && !(fz && std::atoi(fz) == 0)) {
+        bool fuse = q->tmp && !q->user_buf && !(fz && std::atoi(fz) == 0);
+        if (fuse) {
             q->bufs[0] = q->psi;
             q->bufs[1] = q->tmp;
-            const size_t hs = sizeof(cudaIpcMemHandle_t);
-            std::vector<unsigned char> mine(2 * hs), all(2 * hs * world);
-            CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t *>(mine.data()), q->bufs[0]));
-            CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t *>(mine.data() + hs), q->bufs[1]));
-            unsigned char *dh = nullptr;
-            CK(cudaMalloc(&dh, all.size()));
-            CK(cudaMemcpyAsync(dh + (size_t)rank * 2 * hs, mine.data(), 2 * hs, cudaMemcpyHostToDevice, q->st));
-            NK(ncclAllGather(dh + (size_t)rank * 2 * hs, dh, 2 * hs, ncclUint8, q->comm, q->st));
-            CK(cudaMemcpyAsync(all.data(), dh, all.size(), cudaMemcpyDeviceToHost, q->st));
-            CK(cudaStreamSynchronize(q->st));
-            cudaFree(dh);
-            for (int c = 0; c < world; ++c)
-                for (int b = 0; b < 2; ++b) {
-                    if (c == rank) {
-                        q->peer[b][c] = q->bufs[b];
-                        continue;
-                    }
-                    cudaIpcMemHandle_t hnd;
-                    std::memcpy(&hnd, all.data() + ((size_t)c * 2 + b) * hs, hs);
-                    void *ptr = nullptr;
-                    CK(cudaIpcOpenMemHandle(&ptr, hnd, cudaIpcMemLazyEnablePeerAccess));
-                    q->peer[b][c] = (double2 *)ptr;
-                }
+            void *mp[2][8] = {};
+            fuse = q->comm->share(q->bufs[0], bytes, mp[0], q->st);
+            if (fuse && !q->comm->share(q->bufs[1], bytes, mp[1], q->st)) {
+                q->comm->unshare(mp[0]);
+                fuse = false;
+            }
+            for (int b = 0; b < 2 && fuse; ++b)
+                for (int c = 0; c < world; ++c) q->peer[b][c] = (double2 *)mp[b][c];
+        }
+        if (fuse) {
             q->fused_swap = true;
             q->cur = 0;
             // split swap: groups from the top run's bits below the swapped ones
@@ -1294,10 +1087,9 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
                 }
             int seg = 0;  // contiguous top-set bits from a_top (a split top run has two segments)
             while (a_top + seg < q->m && ((tbits >> (a_top + seg)) & 1ull)) ++seg;
-            const char *sz = std::getenv("QSIM_SPLIT_SWAP");
             q->mv_pshift = a_top;
             q->mv_pbits = std::min(std::min(10, seg), std::max(0, q->m - q->g - a_top));
-            q->split = q->mv_pbits > 0 && q->sets.size() > 1 && !(sz && std::atoi(sz) == 0);
+            q->split = q->mv_pbits > 0 && q->sets.size() > 1;
             // default weights: equal shares for every pass of the layer (boundary turning run,
             // plain runs, the 12-bit set).  A non-boundary pass moves its share at almost no cost
             // when the moving tiles are interleaved with local ones; the boundary pass moves per
@@ -1305,7 +1097,6 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
             // whatever its share, so G = 2 used "0,1,1" -- no longer the better choice (below).
             {
                 q->lowswap = lowswap_layout(q->m, q->g) && q->sets.size() >= 3;
-                if (const char *sh = std::getenv("QSIM_LS_SHARE")) q->ls_share = std::max(0.0, std::min(1.0, std::atof(sh)));
             }
             // (re-measured with the final pass kernels: equal shares are best at G = 2 too,
             // 20.7-20.9 vs 22.5 ms per layer with "0,1,1"; profiles/r1_mgpu2_split_weights.jsonl)
@@ -1327,20 +1118,10 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
         }
     }
     q->pending_plus = true;
-    if (const char *e = std::getenv("QSIM_PREFETCH")) q->prefetch = std::atoi(e);
-    if (const char *e = std::getenv("QSIM_L2PROMO")) q->l2promo = std::atoi(e);
-    if (const char *e = std::getenv("QSIM_TMA_STORE")) q->tma_store = std::atoi(e);
-    if (const char *e = std::getenv("QSIM_L2HINT")) q->l2hint = std::atoi(e);
-    if (const char *e = std::getenv("QSIM_ORD_GRP")) q->ord_grp = std::max(0, std::min(4, std::atoi(e)));
-    if (const char *e = std::getenv("QSIM_DEFER")) q->defer = std::atoi(e) != 0;
-    if (const char *e = std::getenv("QSIM_KERNEL")) q->use_tma = std::strcmp(e, "v4") != 0;
-    if (q->use_tma) {
-        CK(qk::setup_tma_kernels());
-        for (const TileSet &S : q->sets)
-            if (!S.tm_ok) q->use_tma = 0;
-    }
-    if (q->f32 && !q->use_tma && q->m > qk::KT)
-        return fail(q, QSIM_EUNSUPPORTED, "QSIM_FP32 needs the TMA pass kernel");
+    if (const char *e = std::getenv("QSIM_TMA_STORE")) q->tma_store = std::atoi(e) != 0;
+    CK(qk::setup_tma_kernels());
+    for (const TileSet &S : q->sets)
+        if (!S.tm_ok) return fail(q, QSIM_EUNSUPPORTED, "tile set without a 5-D TMA view");
     return QSIM_OK;
 }
 
@@ -1374,15 +1155,12 @@ int qsim_destroy(qsim_t *q) {
     if (q->st) cudaStreamSynchronize(q->st);
     if (q->fused_swap) {
         if (q->comm) {  // no rank may unmap while a peer could still write into it
-            ncclAllReduce(q->d_bar, q->d_bar, 1, ncclDouble, ncclSum, q->comm, q->st);
+            q->comm->barrier(q->st);
             cudaStreamSynchronize(q->st);
+            for (int b = 0; b < 2; ++b) q->comm->unshare(reinterpret_cast<void **>(q->peer[b]));
         }
-        for (int b = 0; b < 2; ++b)
-            for (int c = 0; c < q->world; ++c)
-                if (c != q->rank && q->peer[b][c]) cudaIpcCloseMemHandle(q->peer[b][c]);
     }
-    if (q->d_bar) cudaFree(q->d_bar);
-    if (q->comm) ncclCommDestroy(q->comm);
+    delete q->comm;
     if (q->psi && q->psi != q->user_buf) cudaFree(q->psi);
     if (q->tmp && q->tmp != q->user_buf) cudaFree(q->tmp);
     for (int k = 0; k < qsim::NFR; ++k)
@@ -1406,6 +1184,7 @@ int qsim_set_ising(qsim_t *q, const double *h, const double *J) {
     std::vector<double> hh(h, h + n), JJ((size_t)n * n, 0.0);
     for (int i = 0; i < n; ++i) {
         if (!std::isfinite(hh[i])) return fail(q, QSIM_EINVAL, "h contains NaN/Inf");
+        if (J[(size_t)i * n + i] != 0.0) return fail(q, QSIM_EINVAL, "J has a non-zero (or NaN) diagonal entry");
         for (int j = i + 1; j < n; ++j) {
             double v = J[(size_t)i * n + j];
             if (!std::isfinite(v)) return fail(q, QSIM_EINVAL, "J contains NaN/Inf");
@@ -1488,7 +1267,6 @@ int qsim_apply_qsds(qsim_t *q, double tau, int n_steps, const double *s, const d
         if (j > 0 && !(s[j] > s[j - 1])) return fail(q, QSIM_EINVAL, "knots must rise strictly");
     }
     if (s[0] != 0.0 || s[n_knots - 1] != 1.0) return fail(q, QSIM_EINVAL, "knots must span [0, 1]");
-    if (!q->use_tma && q->m > qk::KT) return fail(q, QSIM_EUNSUPPORTED, "QSDS needs the TMA pass kernel");
     const int n = q->n, L = n_steps + 1;  // step operators l = 0..n_steps (eq. AQA4)
     // exact half-step exp[i tau/2 (A X - B h_q Z)] per qubit (AQA3), Z = diag(-1, +1)
     auto half = [&](int l, int a, std::complex<double> (&U)[4]) {
@@ -1537,8 +1315,11 @@ int qsim_apply_qsds(qsim_t *q, double tau, int n_steps, const double *s, const d
 int qsim_apply_hadamard(qsim_t *q, int reps) {
     if (!q) return QSIM_EINVAL;
     if (reps < 1) return fail(q, QSIM_EINVAL, "reps >= 1");
-    if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
-    if (!q->use_tma && q->m > qk::KT) return fail(q, QSIM_EUNSUPPORTED, "needs the TMA pass kernel");
+    if (!q->has_ising && q->J.empty()) {  // no problem data needed: the phase frame is all zero
+        q->h.assign(q->n, 0.0);
+        q->J.assign((size_t)q->n * q->n, 0.0);
+        q->fr_valid = false;
+    }
     const int n = q->n;
     const double r = std::sqrt(0.5);
     std::vector<double2> G((size_t)reps * n * 4);
@@ -1620,12 +1401,18 @@ int qsim_energies(qsim_t *q, uint64_t first, uint64_t count, double *out) {
         int rc = ensure_frame(q);
         if (rc) return rc;
     }
-    qk::ProbeSet PS{};
-    PS.k = std::min(qk::KT, q->m);
-    PS.lmask = 0;
-    for (int i = 0; i < PS.k; ++i) {
-        PS.L[i] = q->m > qk::KT ? q->sets[0].L[i] : i;
-        PS.lmask |= 1ull << PS.L[i];
+    // the hot path's arithmetic: tile records of set 0 (flip 0: energies at the physical labels)
+    // from tile_fields_kernel, then the frame-Z sums of the reducing pass (energy_dump_kernel)
+    qk::PassParams P{};
+    if (q->m > qk::KT) {
+        P = base_params(q, q->sets[0]);
+        P.flip = 0;
+        P.rec = q->d_rec;
+        CK(qk::launch_tile_fields(P, q->d_rec, q->st));
+        q->launches++;
+    } else {
+        P.hp = q->cur_hp;
+        P.Jp = q->cur_Jp;
     }
     const u64 CH = 1ull << 23;
     for (u64 done = 0; done < count; done += CH) {
@@ -1633,9 +1420,9 @@ int qsim_energies(qsim_t *q, uint64_t first, uint64_t count, double *out) {
         int rc = scratch(q, c * sizeof(double));
         if (rc) return rc;
         qk::GatherParams G = gather_params(q, first + done, c, nullptr);
-        CK(qk::launch_energy_probe(G, q->cur_hp, q->cur_Jp, PS, (double *)q->d_scratch,
-                                   (int)std::min<u64>((c + 255) / 256, 4096), q->st));
+        CK(qk::launch_energy_dump(G, P, (double *)q->d_scratch, (int)std::min<u64>((c + 255) / 256, 4096), q->st));
         q->launches++;
+        if (q->world > 1) CM(q->comm->allreduce((double *)q->d_scratch, c, qc::Op::Sum, q->st));
         CK(cudaMemcpyAsync(out + done, q->d_scratch, c * sizeof(double), cudaMemcpyDeviceToHost, q->st));
         CK(cudaStreamSynchronize(q->st));
     }
@@ -1645,7 +1432,6 @@ int qsim_energies(qsim_t *q, uint64_t first, uint64_t count, double *out) {
 int qsim_spin_expectations(qsim_t *q, double *out) {
     if (!q) return QSIM_EINVAL;
     if (!out) return fail(q, QSIM_EINVAL, "out is NULL");
-    if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
     if (q->m <= qk::KT) {  // small states: amplitudes are few; gather and sum in the fixed order
         const u64 dim = 1ull << q->n;
         std::vector<double> amp(2 * dim);
@@ -1671,7 +1457,7 @@ int qsim_spin_expectations(qsim_t *q, double *out) {
     CK(qk::launch_spin(P, part, grid, q->st));
     CK(qk::launch_sum_vec(part, grid, q->n, vec, q->st));
     q->launches += 2;
-    if (q->world > 1) NK(ncclAllReduce(vec, vec, q->n, ncclDouble, ncclSum, q->comm, q->st));
+    if (q->world > 1) CM(q->comm->allreduce(vec, q->n, qc::Op::Sum, q->st));
     std::vector<double> phys(q->n);
     CK(cudaMemcpyAsync(phys.data(), vec, sizeof(double) * q->n, cudaMemcpyDeviceToHost, q->st));
     CK(cudaStreamSynchronize(q->st));
@@ -1705,11 +1491,16 @@ int qsim_ground_states(qsim_t *q, uint64_t *out, int max_out, double *emin_out, 
     const u64 u0 = ntiles * (u64)q->rank / (u64)q->world, u1 = ntiles * (u64)(q->rank + 1) / (u64)q->world;
     const int grid = (int)std::max<u64>(1, std::min<u64>((u64)q->num_sms * 8, u1 - u0));
     const int cap = std::max(max_out, 1);
-    int rc = scratch(q, sizeof(double) * (grid + 1) + sizeof(unsigned long long) * 2 + sizeof(u64) * cap);
+    // collect pass: every CTA keeps the first `cap` minimisers of its tiles (ascending); the
+    // merged lists contain the global first `cap` (per-CTA slots bounded to 2^24 labels)
+    const int cgrid = (int)std::max<u64>(1, std::min<u64>((u64)grid, (1ull << 24) / (u64)cap));
+    int rc = scratch(q, sizeof(double) * (grid + 1) + sizeof(unsigned long long) * 2 + sizeof(unsigned) * cgrid +
+                            sizeof(u64) * (size_t)cap * cgrid + 16);
     if (rc) return rc;
     double *part = (double *)q->d_scratch, *res = part + grid;
     unsigned long long *cnt = (unsigned long long *)(res + 1);
-    u64 *lst = (u64 *)(cnt + 2);
+    unsigned *ccnt = (unsigned *)(cnt + 2);
+    u64 *lst = (u64 *)(((uintptr_t)(ccnt + cgrid) + 15) & ~(uintptr_t)15);
     qk::EnumParams E{};
     E.h = q->d_hlog;
     E.J = q->d_hlog + q->n;
@@ -1721,7 +1512,7 @@ int qsim_ground_states(qsim_t *q, uint64_t *out, int max_out, double *emin_out, 
     CK(qk::launch_enum(E, grid, q->st));
     CK(qk::launch_min_partials(part, grid, res, q->st));
     q->launches += 2;
-    if (q->world > 1) NK(ncclAllReduce(res, res, 1, ncclDouble, ncclMin, q->comm, q->st));
+    if (q->world > 1) CM(q->comm->allreduce(res, 1, qc::Op::Min, q->st));
     double emin = 0.0;
     CK(cudaMemcpyAsync(&emin, res, sizeof(double), cudaMemcpyDeviceToHost, q->st));
     CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), q->st));
@@ -1729,16 +1520,23 @@ int qsim_ground_states(qsim_t *q, uint64_t *out, int max_out, double *emin_out, 
     E.collect = 1;
     E.emin = emin;
     E.out = lst;
+    E.cta_cnt = ccnt;
     E.count = cnt;
     E.max_out = cap;
-    CK(qk::launch_enum(E, grid, q->st));
+    CK(qk::launch_enum(E, cgrid, q->st));
     q->launches++;
     unsigned long long c = 0;
+    std::vector<unsigned> cc(cgrid);
+    std::vector<u64> lists((size_t)cap * cgrid);
     CK(cudaMemcpyAsync(&c, cnt, sizeof(c), cudaMemcpyDeviceToHost, q->st));
+    CK(cudaMemcpyAsync(cc.data(), ccnt, sizeof(unsigned) * cgrid, cudaMemcpyDeviceToHost, q->st));
+    CK(cudaMemcpyAsync(lists.data(), lst, sizeof(u64) * lists.size(), cudaMemcpyDeviceToHost, q->st));
     CK(cudaStreamSynchronize(q->st));
-    std::vector<u64> mine((size_t)std::min<unsigned long long>(c, (unsigned long long)cap));
-    if (!mine.empty()) CK(cudaMemcpy(mine.data(), lst, sizeof(u64) * mine.size(), cudaMemcpyDeviceToHost));
+    std::vector<u64> mine;
+    for (int b = 0; b < cgrid; ++b)
+        for (unsigned k = 0; k < std::min<unsigned>(cc[b], (unsigned)cap); ++k) mine.push_back(lists[(size_t)b * cap + k]);
     std::sort(mine.begin(), mine.end());
+    if (mine.size() > (size_t)cap) mine.resize(cap);
     std::vector<u64> all = mine;
     unsigned long long total = c;
     if (q->world > 1) {  // gather every rank's (count, first cap labels)
@@ -1749,7 +1547,7 @@ int qsim_ground_states(qsim_t *q, uint64_t *out, int max_out, double *emin_out, 
         u64 *d = nullptr;
         CK(cudaMalloc(&d, sizeof(u64) * rec * (1 + q->world)));
         CK(cudaMemcpyAsync(d, sendv.data(), sizeof(u64) * rec, cudaMemcpyHostToDevice, q->st));
-        NK(ncclAllGather(d, d + rec, rec, ncclUint64, q->comm, q->st));
+        CM(q->comm->allgather(d, d + rec, rec * sizeof(u64), q->st));
         CK(cudaMemcpyAsync(recv.data(), d + rec, sizeof(u64) * rec * q->world, cudaMemcpyDeviceToHost, q->st));
         CK(cudaStreamSynchronize(q->st));
         cudaFree(d);
@@ -1853,23 +1651,14 @@ int qsim_plan_positions(int n, int world, int layers, int *pos_out) {
 int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
     if (!q || !ms_out || reps < 1) return QSIM_EINVAL;
     const int ns = (int)q->sets.size();
-    const bool tm = q->tilemajor && set == ns;  // the relabelling schedule's tile shape, out of place
-    if (q->m <= qk::KT || set < 0 || set > ns || (set == ns && !tm)) return fail(q, QSIM_EINVAL, "no such tile set");
+    if (q->m <= qk::KT || set < 0 || set >= ns) return fail(q, QSIM_EINVAL, "no such tile set");
     if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
     int rc = materialize_plus(q);
     if (rc) return rc;
     rc = ensure_frame(q);
     if (rc) return rc;
-    const TileSet &S = tm ? q->tmset : q->sets[set];
+    const TileSet &S = q->sets[set];
     qk::PassParams P = base_params(q, S);
-    if (tm) {  // identity output labelling
-        P.tmo = 1;
-        P.out = q->bufs[q->cur ^ 1];
-        P.onseg = 1;
-        P.oseg_src[0] = 0;
-        P.oseg_len[0] = q->m - qk::KT;
-        P.oseg_dst[0] = 0;
-    }
     std::complex<double> k1, k2;
     P.c1 = mix_coef(0.3, k1);
     P.c2 = mix_coef(-0.2, k2);
@@ -1881,10 +1670,6 @@ int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
     std::complex<double> sc = cpow_int(k1, __builtin_popcount(P.mix1)) * cpow_int(k2, __builtin_popcount(P.mix2));
     P.scale = make_double2(sc.real(), sc.imag());
     P.kind = S.full12 ? (phase ? qk::K_TURN12 : qk::K_PLAIN12) : (phase ? qk::K_TURN_RUN : qk::K_PLAIN_RUN);
-    if (tm) {  // tile-major shape: run passes mix t3..t11; the "12" program mixes all 12
-        P.mix1 = P.mix1 ? 0xFF8u : 0u;
-        P.mix2 = P.mix2 ? 0xFF8u : 0u;
-    }
     P.phase = phase;
     P.gamma = 0.1;
     P.rec = q->d_rec;
@@ -1894,16 +1679,11 @@ int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     int grid = 0;
-    // QSIM_BENCH_OOP=1: out of place (TMA stores into a second buffer, same layout) -- probe of
-    // the DRAM read/write mix of in-place vs ping-pong passes
-    double2 *oop = nullptr;
-    if (const char *e = std::getenv("QSIM_BENCH_OOP"); e && std::atoi(e) == 1 && !tm)
-        CK(cudaMalloc(&oop, q->es << q->m));
-    rc = launch_pass_any(q, S, P, &grid, oop);  // warm-up
+    rc = launch_pass(q, S, P, &grid);  // warm-up
     if (rc) return rc;
     CK(cudaEventRecord(e0, q->st));
     for (int r = 0; r < reps; ++r) {
-        rc = launch_pass_any(q, S, P, &grid, oop);
+        rc = launch_pass(q, S, P, &grid);
         if (rc) return rc;
     }
     CK(cudaEventRecord(e1, q->st));
@@ -1912,7 +1692,6 @@ int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
     CK(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    if (oop) cudaFree(oop);
     q->res_valid = false;
     *ms_out = ms / reps;
     return QSIM_OK;
@@ -1923,6 +1702,7 @@ int qsim_profile_enable(qsim_t *q, int on) {
     q->prof = on != 0;
     q->ev_used = 0;
     q->prof_bytes.clear();
+    q->prof_kind.clear();
     return QSIM_OK;
 }
 
@@ -1942,10 +1722,11 @@ int qsim_profile_read(qsim_t *q, double *ms_sum, uint64_t *count, double *bytes_
     *bytes_sum = by;
     q->ev_used = 0;
     q->prof_bytes.clear();
+    q->prof_kind.clear();
     return QSIM_OK;
 }
 
-int qsim_profile_passes(qsim_t *q, double *ms_out, int cap) {
+int qsim_profile_passes(qsim_t *q, double *ms_out, int *kind_out, int cap) {
     if (!q || (cap > 0 && !ms_out)) return QSIM_EINVAL;
     CK(cudaStreamSynchronize(q->st));
     const int npass = (int)(q->ev_used / 2);
@@ -1953,17 +1734,33 @@ int qsim_profile_passes(qsim_t *q, double *ms_out, int cap) {
         float t = 0.f;
         CK(cudaEventElapsedTime(&t, q->ev_pool[2 * i], q->ev_pool[2 * i + 1]));
         ms_out[i] = t;
+        if (kind_out) kind_out[i] = q->prof_kind[i];
     }
     q->ev_used = 0;
     q->prof_bytes.clear();
+    q->prof_kind.clear();
     return npass;
 }
 
 uint64_t qsim_kernel_launches(const qsim_t *q) { return q ? q->launches : 0; }
 
+int qsim_num_qubits(const qsim_t *q) { return q ? q->n : QSIM_EINVAL; }
+
+int qsim_swap_path(const qsim_t *q) {
+    if (!q) return QSIM_EINVAL;
+    if (q->world == 1) return QSIM_SWAP_NONE;
+    if (q->fused_swap) return q->lowswap ? QSIM_SWAP_LOWBIT : (q->split ? QSIM_SWAP_FUSED_SPLIT : QSIM_SWAP_FUSED);
+    return q->tmp ? QSIM_SWAP_COLLECTIVE : QSIM_SWAP_INPLACE_STAGED;
+}
+
 const char *qsim_last_error(const qsim_t *q) { return q ? q->err.c_str() : g_create_error.c_str(); }
 
 const char *qsim_version(void) { return "qsim-b200 0.2 (sm_100a, FP64 + FP32 mode)"; }
+
+int qsim_loopback_id(int world, void *out128) {
+    if (!out128 || world < 1 || world > 8 || ilog2(world) < 0) return QSIM_EINVAL;
+    return qc::make_loopback_id(world, out128) == 0 ? QSIM_OK : QSIM_EINVAL;
+}
 
 int qsim_nccl_unique_id(void *out128) {
     if (!out128) return QSIM_EINVAL;

@@ -90,9 +90,10 @@ __global__ void sum_vec_kernel(const double *part, int nparts, int n, double *ou
 // Tiles of 4096 consecutive labels z (bits 0..11); frame X gives every thread 32 labels that
 // differ in bits 7..11.  Per tile the CTA computes h'_i (i < 12) and E_H with the shared
 // energy functions; per thread E_j = base + tree over 5 register bits + E_RR(j).
+constexpr int EMAX = 48;  // qsim_enumerate accepts n <= 48 (the state-carrying handles n <= NMAX)
 struct EnumCtx {
     double hL[KT];
-    double ehp[NMAX];
+    double ehp[EMAX];
 };
 
 __device__ __forceinline__ void enum_tile(const EnumParams &E, EnumCtx &c, u64 u, const ThreadEnergy &te,
@@ -122,35 +123,74 @@ __device__ __forceinline__ void enum_tile(const EnumParams &E, EnumCtx &c, u64 u
     __syncthreads();  // hL / ehp reused by the next tile
 }
 
+// collect pass: every CTA writes the first max_out minimisers of its tiles in ascending label
+// order to out[blockIdx.x * max_out ..] (its tiles ascend, and inside a tile the label order is
+// (j, warp, lane) -- register bits 7..11 above the thread bits 0..6 -- which the ballot prefix
+// below follows), and the number written to cta_cnt[blockIdx.x].  The host merges the per-CTA
+// lists: the global first max_out minimisers are among them.  count += all minimisers.
 __global__ void __launch_bounds__(NTHR) enum_kernel(const EnumParams E) {
     __shared__ EnumCtx c;
     __shared__ double eRR[NR];
     __shared__ double red[NTHR / 32];
+    __shared__ int wc[NTHR / 32];
+    __shared__ int stored;
+    __shared__ unsigned long long tot_sh[NTHR / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int L[KT];
 #pragma unroll
     for (int i = 0; i < KT; ++i) L[i] = i;
     const ThreadEnergy te = thread_energy<FX>(E.J, E.n, L, lane, warp, 0);
     if (tid < NR) eRR[tid] = err_of<FX>(E.J, E.n, L, tid);
+    if (tid == 0) stored = 0;
     __syncthreads();
     const int tX = Frame<FX>::tthr(lane, warp);
     double emin = 1.0e300;
+    unsigned long long tot = 0;
     double Q[NR];
+    u64 *const out = E.collect ? E.out + (size_t)blockIdx.x * (size_t)E.max_out : nullptr;
     for (u64 u = E.u0 + blockIdx.x; u < E.u1; u += gridDim.x) {
         enum_tile(E, c, u, te, eRR, tX, Q);
         if (E.collect) {
+            unsigned mm = 0;
 #pragma unroll
-            for (int j = 0; j < NR; ++j)
-                if (Q[j] == E.emin) {
-                    const unsigned long long k = atomicAdd(E.count, 1ull);
-                    if (k < (unsigned long long)E.max_out) E.out[k] = (u << KT) | (u64)(tX | (j << Frame<FX>::RB));
+            for (int j = 0; j < NR; ++j) mm |= (Q[j] == E.emin) ? (1u << j) : 0u;
+            tot += __popc(mm);
+            if (!__syncthreads_or(mm != 0u) || stored >= E.max_out) continue;  // block-uniform
+            for (int j = 0; j < NR; ++j) {
+                const bool f = (mm >> j) & 1u;
+                if (!__syncthreads_or(f)) continue;
+                const unsigned b = __ballot_sync(0xffffffffu, f);
+                if (lane == 0) wc[warp] = __popc(b);
+                __syncthreads();
+                int before = stored + __popc(b & ((1u << lane) - 1u));
+                for (int w = 0; w < warp; ++w) before += wc[w];
+                if (f && before < E.max_out) out[before] = (u << KT) | (u64)(tX | (j << Frame<FX>::RB));
+                __syncthreads();
+                if (tid == 0) {
+                    int s = stored;
+                    for (int w = 0; w < NTHR / 32; ++w) s += wc[w];
+                    stored = s;
                 }
+                __syncthreads();
+                if (stored >= E.max_out) break;
+            }
         } else {
 #pragma unroll
             for (int j = 0; j < NR; ++j) emin = fmin(emin, Q[j]);
         }
     }
-    if (!E.collect) {
+    if (E.collect) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (lane == 0) tot_sh[warp] = tot;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < NTHR / 32; ++w) t += tot_sh[w];
+            if (t) atomicAdd(E.count, t);
+            E.cta_cnt[blockIdx.x] = (unsigned)min(stored, E.max_out);
+        }
+    } else {
 #pragma unroll
         for (int o = 16; o; o >>= 1) emin = fmin(emin, __shfl_xor_sync(0xffffffffu, emin, o));
         if (lane == 0) red[warp] = emin;

@@ -91,16 +91,15 @@ __device__ __forceinline__ double eh_term(const double *hp, const double *Jp, in
     return spin(X, j) * acc;
 }
 
-// E(X) for one full physical index X, composed from the same pieces (probe kernel).
-__device__ inline double energy_point(const double *hp, const double *Jp, int n, const int *L, int k,
-                               u64 lmask, u64 X) {
+// E(X) summed directly (fields i ascending, each followed by its couplings j > i): the small-state
+// kernel's energy (m <= 12), also read back by qsim_energies for such states.
+__device__ __forceinline__ double energy_direct(const double *hp, const double *Jp, int n, u64 X) {
     double e = 0.0;
-    for (int j = 0; j < n; ++j)
-        if (!((lmask >> j) & 1ull)) e += eh_term(hp, Jp, n, j, X, lmask);
-    for (int i = 0; i < k; ++i) e += spin(X, L[i]) * field_hprime(hp, Jp, n, L[i], X, lmask);
-    for (int i = 0; i < k; ++i)
-        for (int i2 = i + 1; i2 < k; ++i2)
-            e += Jp[L[i] * n + L[i2]] * spin(X, L[i]) * spin(X, L[i2]);
+    for (int i = 0; i < n; ++i) {
+        const double si = spin(X, i);
+        e += hp[i] * si;
+        for (int j = i + 1; j < n; ++j) e += Jp[i * n + j] * si * spin(X, j);
+    }
     return e;
 }
 

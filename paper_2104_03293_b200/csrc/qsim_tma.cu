@@ -55,25 +55,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-// L2 cache policy for the streamed state (QSIM_L2HINT: 0 none, 1 evict_first, 2 evict_last)
-__device__ __forceinline__ uint64_t l2_policy(int kind) {
-    uint64_t pol = 0;
-    if (kind == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    else if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *tm, const int (&c)[5], uint64_t *bar,
-                                            int hint = 0) {
-    if (hint) {
-        const uint64_t pol = l2_policy(hint);
-        asm volatile(
-            "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(dst)),
-            "l"(reinterpret_cast<uint64_t>(tm)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]),
-            "r"(smem_u32(bar)), "l"(pol)
-            : "memory");
-        return;
-    }
+__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *tm, const int (&c)[5], uint64_t *bar) {
     asm volatile(
         "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
@@ -88,22 +70,12 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
         "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ void tma_store_5d(const CUtensorMap *tm, const int (&c)[5], const void *src,
-                                             int hint = 0) {
-    if (hint) {
-        const uint64_t pol = l2_policy(hint);
-        asm volatile(
-            "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4, %5}], [%6], %7;" ::
-                "l"(reinterpret_cast<uint64_t>(tm)),
-            "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(src)), "l"(pol)
-            : "memory");
-    } else {
-        asm volatile(
-            "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
-                reinterpret_cast<uint64_t>(tm)),
-            "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(src))
-            : "memory");
-    }
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap *tm, const int (&c)[5], const void *src) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+            reinterpret_cast<uint64_t>(tm)),
+        "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(src))
+        : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
@@ -153,11 +125,8 @@ __device__ __forceinline__ u64 tile_of(const PassParams &P, u64 k) {
     return ((k << P.ord_rot) | (k >> (P.ord_bits - P.ord_rot))) & mask;
 }
 
-// global sequence index of the CTA's i-th tile (cyclic over CTAs in groups of 2^ord_grp)
-__device__ __forceinline__ u64 seq_of(const PassParams &P, u64 i) {
-    const int q = P.ord_grp;
-    return ((blockIdx.x + (i >> q) * (u64)gridDim.x) << q) + (i & ((1ull << q) - 1ull));
-}
+// global sequence index of the CTA's i-th tile (cyclic over CTAs)
+__device__ __forceinline__ u64 seq_of(const PassParams &, u64 i) { return blockIdx.x + i * (u64)gridDim.x; }
 
 template <int MV>
 __device__ __forceinline__ void issue_tile(const PassParams &P, const TmaIssue &I, u64 i, int s, bool load_state,
@@ -174,7 +143,7 @@ __device__ __forceinline__ void issue_tile(const PassParams &P, const TmaIssue &
 #pragma unroll
         for (int d = 0; d < 5; ++d)
             c[d] = P.tm_clen[d] ? (int)((ut >> P.tm_cshift[d]) & ((1ull << P.tm_clen[d]) - 1ull)) : 0;
-        tma_load_5d(I.stages + (size_t)s * SM_TILE_BYTES, I.tm, c, &I.full[s], P.l2hint & 3);
+        tma_load_5d(I.stages + (size_t)s * SM_TILE_BYTES, I.tm, c, &I.full[s]);
     }
     if (load_rec) bulk_load(I.srec + s, I.grec + ut, (uint32_t)TILE_REC_BYTES, &I.full[s]);
     __threadfence_block();
@@ -193,18 +162,6 @@ __device__ __forceinline__ void wait_tile(const TmaIssue &I, u64 i) {
 }
 
 constexpr unsigned TMX = 0xF80u, TMY = 0x01Fu, TMZ = 0x060u, TMW = 0x078u;
-
-// tile-major out-of-place store: the tile is written as one contiguous 64 KiB block (element
-// t at t), so every warp store covers >= 128 contiguous bytes and every CTA writes whole blocks
-template <int F, typename V>
-__device__ __forceinline__ void store_tile_major(const V (&v)[NR], const PassParams &P, u64 ut, int lane,
-                                                 int warp) {
-    u64 ou = 0;
-    for (int k = 0; k < P.onseg; ++k) ou |= ((ut >> P.oseg_src[k]) & ((1ull << P.oseg_len[k]) - 1ull)) << P.oseg_dst[k];
-    V *base = reinterpret_cast<V *>(P.out) + (ou << KT) + Frame<F>::tthr(lane, warp);
-#pragma unroll
-    for (int j = 0; j < NR; ++j) __stcs(base + (j << Frame<F>::RB), v[j]);
-}
 
 // store with the fused global-qubit swap: local index x = (c | y) with c the top
 // g local bits goes to rank c's other buffer at (rank | y); 1/G of the stores stay local, the
@@ -276,8 +233,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     const int n = P.n;
     const bool need_e = TURN || P.reduce;
     const bool load_state = !(TURN && P.init) && !(P.dbg & 2);
-    const u64 ngrp = P.ntiles >> P.ord_grp;
-    const u64 ntl = ((ngrp > blockIdx.x) ? (ngrp - blockIdx.x + gridDim.x - 1) / gridDim.x : 0) << P.ord_grp;
+    const u64 ntl = (P.ntiles > blockIdx.x) ? (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     volatile int *issued = reinterpret_cast<volatile int *>(smem + TmaSmem::iss_off);
     const TmaIssue I{&tmap, MV ? &smap : &tmap, reinterpret_cast<const TileRec *>(P.rec), stages, (uint32_t)(TILE * sizeof(V)),
                      srec, full, issued};
@@ -340,7 +296,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     V v[NR];
     long long pend = -1;  // tile whose TMA store still reads its stage (deferred refill)
     int pend_s = 0;
-    // deferred refill (P.defer): the TMA store of the group's previous tile is left running and
+    // deferred refill: the TMA store of the group's previous tile is left running and
     // its stage is refilled after this tile's first frame load, so the elected thread does not
     // stall its warp (and the group's next barrier) on the store
     auto refill_pending = [&]() {
@@ -401,7 +357,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                                      (sizeof(V) == 16 && MV != 2) ? P.PRR : cs.PRR, cs.PRRf, skW);
                 }
                 if (stp == 3) {  // last smem read done: release the stage unless TMA-storing
-                    if (!(P.tma_store && !(MV && P.swap_store) && !P.tmo)) {
+                    if (!(P.tma_store && !(MV && P.swap_store))) {
                         fence_async_smem();
                         group_bar(g);
                         if (gt == 0 && i + NSTAGE < ntl)
@@ -418,7 +374,6 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 }
                 store_lowswap<FX>(v, P, tb + offX, 0);
             } else if (MV && P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
-            else if (P.tmo) store_tile_major<FX>(v, P, ut, lane, warp);
             else if (P.tma_store) {
                 sts_frame<FX>(v, sm, lane, warp);
                 fence_async_smem();
@@ -426,14 +381,9 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 if (gt == 0) {
                     int c[5];
                     tile_coords(P, ut, c);
-                    tma_store_5d(I.tms, c, sm, (P.l2hint >> 2) & 3);
-                    if (P.defer) {
-                        pend = (long long)i;
-                        pend_s = s;
-                    } else {
-                        bulk_wait_read0();
-                        if (i + NSTAGE < ntl) issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
-                    }
+                    tma_store_5d(I.tms, c, sm);
+                    pend = (long long)i;
+                    pend_s = s;
                 }
             } else
                 store_tile<FX>(v, OUTB + tb + offX, P.L);
@@ -486,7 +436,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         // ------------------------------------------------ release the stage, refill it
         // (a reducing pass reads the stage's tile record, so it finishes before the refill)
         // TMA-store mode keeps the stage until the store has read it back
-        const bool tstore = P.tma_store && !(MV && P.swap_store) && !P.tmo && !(P.dbg & 1);
+        const bool tstore = P.tma_store && !(MV && P.swap_store) && !(P.dbg & 1);
         const bool late_release = (!TURN && P.reduce) || tstore;
         if (!late_release) {
             fence_async_smem();
@@ -498,7 +448,6 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         if (TURN) {
             MIXF(FX, P.mix2 & TMX, 2);
             if (MV && P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
-            else if (P.tmo) store_tile_major<FX>(v, P, ut, lane, warp);
             else if (tstore) {
                 sts_frame<FX>(v, sm, lane, warp);
                 fence_async_smem();
@@ -506,7 +455,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 if (gt == 0) {
                     int c[5];
                     tile_coords(P, ut, c);
-                    tma_store_5d(I.tms, c, sm, (P.l2hint >> 2) & 3);
+                    tma_store_5d(I.tms, c, sm);
                     bulk_wait_read0();
                     if (i + NSTAGE < ntl) issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
                 }
@@ -562,14 +511,9 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 if (gt == 0) {
                     int c[5];
                     tile_coords(P, ut, c);
-                    tma_store_5d(I.tms, c, sm, (P.l2hint >> 2) & 3);
-                    if (P.defer) {
-                        pend = (long long)i;
-                        pend_s = s;
-                    } else {
-                        bulk_wait_read0();
-                        if (i + NSTAGE < ntl) issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
-                    }
+                    tma_store_5d(I.tms, c, sm);
+                    pend = (long long)i;
+                    pend_s = s;
                 }
                 continue;
             }
@@ -579,8 +523,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 if (gt == 0 && i + NSTAGE < ntl)
                     issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
             }
-            if (P.tmo) store_tile_major<RUN ? FRN : FZ>(v, P, ut, lane, warp);
-            else store_tile<RUN ? FRN : FZ>(v, OUTB + tb + offS, P.L, skE);
+            store_tile<RUN ? FRN : FZ>(v, OUTB + tb + offS, P.L, skE);
         }
         }  // generic body
     }

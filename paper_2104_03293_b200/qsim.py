@@ -27,7 +27,8 @@ QSIM_ECUDA = -6
 QSIM_ENCCL = -7
 QSIM_FP64 = 0
 QSIM_FP32 = 1
-QSIM_FP32 = 1
+QSIM_SWAP_NONE, QSIM_SWAP_FUSED_SPLIT, QSIM_SWAP_FUSED, QSIM_SWAP_LOWBIT = 0, 1, 2, 3
+QSIM_SWAP_COLLECTIVE, QSIM_SWAP_INPLACE_STAGED = 4, 5
 
 _ERRNAMES = {QSIM_EINVAL: "EINVAL", QSIM_ENOMEM: "ENOMEM", QSIM_ERANGE: "ERANGE",
              QSIM_ESTATE: "ESTATE", QSIM_EUNSUPPORTED: "EUNSUPPORTED", QSIM_ECUDA: "ECUDA",
@@ -38,7 +39,8 @@ EXPORTS = ["qsim_create", "qsim_create_ex", "qsim_destroy", "qsim_set_ising", "q
            "qsim_apply_qaoa", "qsim_apply_aqa", "qsim_apply_qsds", "qsim_apply_hadamard", "qsim_aqa_angles", "qsim_expect_hc", "qsim_norm2",
            "qsim_success_prob", "qsim_get_amplitudes", "qsim_energies", "qsim_spin_expectations",
            "qsim_apply_aqa_traced", "qsim_ground_states", "qsim_enumerate", "qsim_sync",
-           "qsim_plan_counts", "qsim_plan_positions", "qsim_nccl_unique_id",
+           "qsim_plan_counts", "qsim_plan_positions", "qsim_nccl_unique_id", "qsim_loopback_id",
+           "qsim_swap_path", "qsim_num_qubits",
            "qsim_bench_pass", "qsim_profile_enable", "qsim_profile_read", "qsim_profile_passes", "qsim_kernel_launches", "qsim_last_error",
            "qsim_version"]
 
@@ -83,10 +85,13 @@ lib.qsim_plan_counts.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctype
                                  ctypes.POINTER(ctypes.c_int), _U64]
 lib.qsim_plan_positions.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
 lib.qsim_nccl_unique_id.argtypes = [ctypes.c_void_p]
+lib.qsim_loopback_id.argtypes = [ctypes.c_int, ctypes.c_void_p]
+lib.qsim_swap_path.argtypes = [_H]
+lib.qsim_num_qubits.argtypes = [_H]
 lib.qsim_bench_pass.argtypes = [_H, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D]
 lib.qsim_profile_enable.argtypes = [_H, ctypes.c_int]
 lib.qsim_profile_read.argtypes = [_H, _D, _U64, _D]
-lib.qsim_profile_passes.argtypes = [_H, _D, ctypes.c_int]
+lib.qsim_profile_passes.argtypes = [_H, _D, ctypes.POINTER(ctypes.c_int), ctypes.c_int]
 lib.qsim_kernel_launches.argtypes = [_H]
 lib.qsim_kernel_launches.restype = ctypes.c_uint64
 lib.qsim_last_error.argtypes = [_H]
@@ -201,15 +206,15 @@ def qsim_energies(h, first: int, count: int) -> np.ndarray:
     return out
 
 
-def qsim_spin_expectations(h, n: int) -> np.ndarray:
-    out = np.empty(n)
+def qsim_spin_expectations(h) -> np.ndarray:
+    out = np.empty(qsim_num_qubits(h))
     _check(lib.qsim_spin_expectations(h, _dp(out)), h)
     return out
 
 
-def qsim_apply_aqa_traced(h, n: int, T: float, p: int, s, A, B) -> np.ndarray:
+def qsim_apply_aqa_traced(h, T: float, p: int, s, A, B) -> np.ndarray:
     s, A, B = _f64(s), _f64(A), _f64(B)
-    tr = np.empty((p, n))
+    tr = np.empty((p, qsim_num_qubits(h)))
     _check(lib.qsim_apply_aqa_traced(h, float(T), int(p), _dp(s), _dp(A), _dp(B), int(s.shape[0]), _dp(tr)), h)
     return tr
 
@@ -261,6 +266,26 @@ def qsim_nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def qsim_loopback_id(world: int) -> bytes:
+    """128-byte group id of the in-process loopback transport (world ranks = threads of this
+    process on the current device, each passing the id to qsim_create_ex)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.qsim_loopback_id(int(world), buf))
+    return buf.raw
+
+
+def qsim_swap_path(h) -> int:
+    rc = lib.qsim_swap_path(h)
+    _check(min(rc, 0), h)
+    return rc
+
+
+def qsim_num_qubits(h) -> int:
+    rc = lib.qsim_num_qubits(h)
+    _check(min(rc, 0), h)
+    return rc
+
+
 def qsim_bench_pass(h, set_index: int, phase: int, reps: int = 5) -> float:
     out = ctypes.c_double()
     _check(lib.qsim_bench_pass(h, int(set_index), int(phase), int(reps), ctypes.byref(out)), h)
@@ -279,12 +304,19 @@ def qsim_profile_read(h):
     return ms.value, cnt.value, by.value
 
 
-def qsim_profile_passes(h, cap: int = 4096):
-    """-> per-pass durations (ms) of the recorded passes, in launch order"""
+QSIM_PASS_PLAIN12, QSIM_PASS_PLAIN_RUN, QSIM_PASS_TURN12, QSIM_PASS_TURN_RUN = 0, 1, 2, 3
+QSIM_PASS_MOVING, QSIM_PASS_INIT, QSIM_PASS_REDUCE = 4, 8, 16
+
+
+def qsim_profile_passes(h, cap: int = 4096, kinds: bool = False):
+    """-> per-pass durations (ms) of the recorded passes, in launch order (and, with kinds=True,
+    their pass programs: QSIM_PASS_* codes)"""
     out = np.zeros(cap)
-    rc = lib.qsim_profile_passes(h, out.ctypes.data_as(_D), cap)
+    kd = np.zeros(cap, dtype=np.int32)
+    rc = lib.qsim_profile_passes(h, out.ctypes.data_as(_D), kd.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), cap)
     _check(min(rc, 0), h)
-    return out[: min(rc, cap)].copy()
+    k = min(rc, cap)
+    return (out[:k].copy(), kd[:k].copy()) if kinds else out[:k].copy()
 
 
 def qsim_kernel_launches(h) -> int:
@@ -302,7 +334,9 @@ def qsim_version() -> str:
 # ------------------------------------------------------------------ convenience wrapper
 class QSim:
     """One state-vector handle.  Single GPU: QSim(n).  Multi-GPU (SPMD, one process
-    per GPU): QSim(n, rank=r, world=G, nccl_unique_id=uid)."""
+    per GPU): QSim(n, rank=r, world=G, nccl_unique_id=uid).  Loopback test transport (G
+    threads of one process on one device): nccl_unique_id=qsim_loopback_id(G), one thread per
+    rank."""
 
     def __init__(self, n: int, rank: int = 0, world: int = 1, nccl_unique_id: bytes | None = None,
                  state_buf: int | None = None, buf_bytes: int = 0, cuda_stream: int | None = None,
@@ -372,16 +406,20 @@ class QSim:
         return qsim_energies(self.h, first, count)
 
     def spins(self):
-        return qsim_spin_expectations(self.h, self.n)
+        return qsim_spin_expectations(self.h)
 
     def apply_aqa_traced(self, T, p, s, A, B):
-        return qsim_apply_aqa_traced(self.h, self.n, T, p, s, A, B)
+        return qsim_apply_aqa_traced(self.h, T, p, s, A, B)
 
     def ground_states(self, max_out=64):
         return qsim_ground_states(self.h, max_out)
 
     def sync(self):
         qsim_sync(self.h)
+
+    @property
+    def swap_path(self):
+        return qsim_swap_path(self.h)
 
     @property
     def launches(self):

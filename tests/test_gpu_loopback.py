@@ -1,0 +1,123 @@
+"""Multi-GPU swap paths on ONE GPU: the G ranks
+of a sharded handle are threads of this process (the loopback transport of qsim_loopback_id),
+each with its own shard buffers and stream.  The engine, the pass kernels with their peer
+stores, the split-swap group ranges and the permutation / flip bookkeeping are the NCCL path's;
+only the transport differs.  Every swap path runs here: fused split (default), collective
+(QSIM_FUSED_SWAP=0), in-place staged (QSIM_SWAP_INPLACE=1, the n = 36 path), low-bit
+(QSIM_LOWSWAP=1) and non-default split weights (QSIM_SPLIT_W), against the oracle (full
+state at n <= 24, structured pins P4/P8/P9 at n = 31, 32)."""
+from __future__ import annotations
+
+import threading
+
+import pytest
+
+from tests.sharded_checks import run_checks
+
+pytestmark = pytest.mark.gpu
+
+
+def _q():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2104_03293_b200 import qsim as Q
+
+    return Q
+
+
+class _Ids:
+    """fresh loopback group id per handle, shared by the world rank threads (k-th handle of
+    every rank gets the k-th id)"""
+
+    def __init__(self, Q, world):
+        self.Q, self.world, self.lock, self.ids, self.count = Q, world, threading.Lock(), {}, [0] * world
+
+    def get(self, rank):
+        k = self.count[rank]
+        self.count[rank] += 1
+        with self.lock:
+            if k not in self.ids:
+                self.ids[k] = self.Q.qsim_loopback_id(self.world)
+            return self.ids[k]
+
+
+def run_loopback(world, body, timeout=1500):
+    """run body(rank, new_sim) on `world` threads; returns rank 0's result, re-raises errors"""
+    Q = _q()
+    ids = _Ids(Q, world)
+    res, errs = [None] * world, []
+
+    def worker(rank):
+        try:
+            def new_sim(n, precision=Q.QSIM_FP64):
+                return Q.QSim(n, rank=rank, world=world, nccl_unique_id=ids.get(rank), precision=precision)
+
+            res[rank] = body(rank, new_sim)
+        except BaseException as e:  # noqa: BLE001
+            errs.append((rank, repr(e)))
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout)
+    assert not any(t.is_alive() for t in th), "loopback ranks hung"
+    assert not errs, errs
+    return res[0]
+
+
+def _check(world, n, expect_path, p=3, full=True, extras=True):
+    out = run_loopback(world, lambda r, ns: run_checks(r, world, ns, n, p=p, full=full, extras=extras))
+    paths = [d for (nm, ok, d) in out if nm.endswith("swap path")]
+    assert paths and int(paths[0]) == expect_path, (paths, expect_path)
+    bad = [(nm, d) for (nm, ok, d) in out if not ok]
+    assert not bad, bad
+    assert len(out) >= 5
+
+
+@pytest.mark.parametrize("world,n", [(2, 18), (2, 24), (4, 20), (4, 24)])
+def test_loopback_fused_split(world, n):
+    Q = _q()
+    _check(world, n, Q.QSIM_SWAP_FUSED_SPLIT)
+
+
+@pytest.mark.parametrize("world,n", [(2, 20), (4, 21)])
+def test_loopback_collective_swap(world, n, monkeypatch):
+    Q = _q()
+    monkeypatch.setenv("QSIM_FUSED_SWAP", "0")
+    _check(world, n, Q.QSIM_SWAP_COLLECTIVE, extras=False)
+
+
+@pytest.mark.parametrize("world,n", [(2, 20), (4, 22), (2, 24)])
+def test_loopback_inplace_staged_swap(world, n, monkeypatch):
+    Q = _q()
+    monkeypatch.setenv("QSIM_SWAP_INPLACE", "1")
+    _check(world, n, Q.QSIM_SWAP_INPLACE_STAGED, extras=(n == 24))
+
+
+@pytest.mark.parametrize("n", [23, 24])
+def test_loopback_lowbit_swap(n, monkeypatch):
+    Q = _q()
+    monkeypatch.setenv("QSIM_LOWSWAP", "1")
+    _check(2, n, Q.QSIM_SWAP_LOWBIT, p=4, extras=False)
+
+
+def test_loopback_split_weights(monkeypatch):
+    Q = _q()
+    monkeypatch.setenv("QSIM_SPLIT_W", "0,1,2")  # n = 24, G = 2: 3 passes per layer
+    _check(2, 24, Q.QSIM_SWAP_FUSED_SPLIT, extras=False)
+
+
+@pytest.mark.parametrize("world,n", [(2, 31), (4, 32)])
+def test_loopback_full_size_structured(world, n):
+    """the bench's per-GPU shard (2^30 amplitudes per rank) on the fused split path: p = 1
+    closed-form <H_C>, energies, cluster (P9) and product (P8) amplitudes spanning global bits"""
+    import torch
+
+    need = world * 2 * 16 * (1 << (n - (world.bit_length() - 1))) + (8 << 30)
+    if torch.cuda.mem_get_info()[0] < need:
+        pytest.skip("not enough device memory for the loopback shards")
+    Q = _q()
+    _check(world, n, Q.QSIM_SWAP_FUSED_SPLIT, p=3, full=False, extras=False)

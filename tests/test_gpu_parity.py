@@ -521,3 +521,84 @@ def test_set_ising_twice_and_reuse(Q):
     ref = o.qaoa_state(h2, J2, g, b)
     assert_state_close(psi, ref)
     assert_expect_close(e, h2, J2, ref)
+
+
+# ------------------------------------------------------------------ NEXT-3: more minimisers than max_out
+@pytest.mark.parametrize("n,zeros,max_out", [(16, 6, 5), (20, 9, 37), (17, 17, 3)])
+def test_ground_states_first_minimisers_when_count_exceeds_max_out(Q, n, zeros, max_out):
+    """qsim.h promises the first max_out minimisers in ascending label order.  A product
+    instance (J = 0) with `zeros` zero fields has 2^zeros minimisers (brute force by the
+    oracle); the smallest max_out labels must come back whatever the CTA scheduling order."""
+    rng = np.random.default_rng(n + zeros)
+    h = rng.choice([-1.5, -0.5, 0.5, 1.0], size=n)
+    h[rng.permutation(n)[:zeros]] = 0.0
+    J = np.zeros((n, n))
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        gs, emin, cnt = s.ground_states(max_out=max_out)
+    rgs, remin, rcnt = o.ground_states(h, J, max_out=max_out)
+    assert cnt == rcnt == 2 ** zeros and emin == remin == -np.sum(np.abs(h))
+    assert gs == rgs == sorted(gs) and len(gs) == max_out
+
+
+def test_enumerate_beyond_40_qubits(Q):
+    """qsim_enumerate at n = 41 (the state-less entry accepts n <= 48): a J = 0 product instance
+    has the unique minimiser z_i = [h_i < 0] and E_min = -sum |h| (closed form, brute force not
+    needed); one coupled pair checks the couplings at positions >= 40."""
+    n = 41
+    rng = np.random.default_rng(41)
+    h = rng.choice([-2.0, -1.0, -0.5, 0.5, 1.0, 2.0], size=n)
+    J = np.zeros((n, n))
+    gs, emin, cnt, ms = Q.qsim_enumerate(h, J, max_out=4)
+    z = sum(1 << i for i in range(n) if h[i] < 0)
+    assert cnt == 1 and gs == [z] and emin == -np.sum(np.abs(h))
+    # couple qubits 39 and 40 antiferromagnetically with a field-free pair: E_min gains -|J|
+    h2 = h.copy()
+    h2[39] = h2[40] = 0.0
+    J2 = np.zeros((n, n))
+    J2[39, 40] = 3.0
+    gs2, emin2, cnt2, _ = Q.qsim_enumerate(h2, J2, max_out=4)
+    base = sum(1 << i for i in range(39) if h2[i] < 0)
+    assert cnt2 == 2 and emin2 == -np.sum(np.abs(h2)) - 3.0
+    assert gs2 == sorted([base | (1 << 39), base | (1 << 40)])
+
+
+def test_boundary_errors_and_hadamard_without_problem(Q):
+    """J with a non-zero diagonal is EINVAL (eq:HC has no self-coupling); the
+    Hadamard benchmark needs no problem data."""
+    n = 14
+    h, J = inst.random_ising(n, 3)
+    Jd = J.copy()
+    Jd[2, 2] = 0.5
+    with Q.QSim(n) as s:
+        with pytest.raises(Q.QsimError) as ei:
+            s.set_ising(h, Jd)
+        assert ei.value.code == Q.QSIM_EINVAL
+        s.init_plus()
+        s.apply_hadamard(2)  # H^2 = I: |+> comes back
+        psi = s.amplitudes()
+        assert Q.qsim_num_qubits(s.h) == n and s.spins().shape == (n,)
+    assert np.max(np.abs(psi - 2.0 ** (-n / 2))) <= 1e-14
+
+
+@pytest.mark.parametrize("n", [13, 22])
+def test_energies_are_the_reducing_pass_energies(Q, n):
+    """qsim_energies returns E(z) from the hot path's own arithmetic (tile records + the frame-Z
+    register tree of the reducing pass).  With a non-dyadic instance (bit-exactness not claimed,
+    reading R14) the sum over |psi|^2 E of the returned energies must reproduce the fused
+    <H_C> of the last pass to rounding, and every E(z) the oracle's to 1e-12 relative."""
+    rng = np.random.default_rng(n)
+    h = rng.normal(size=n)
+    J = np.triu(rng.normal(size=(n, n)), 1)
+    g, b = rand_angles(3, n)
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        s.init_plus()
+        s.apply_qaoa(g, b)
+        e_fused = s.expect_hc()
+        psi = s.amplitudes()
+        en = s.energies()
+    ref = o.energies(h, J)
+    assert np.max(np.abs(en - ref)) <= 1e-12 * np.max(np.abs(ref))
+    p = np.abs(psi) ** 2
+    assert abs(np.dot(p, en) - e_fused) <= 1e-11 * np.dot(p, np.abs(en))
