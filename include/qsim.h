@@ -212,9 +212,16 @@ int qsim_loopback_id(int world, void *out128);
  *   QSIM_SWAP_FUSED           the same, all moved by the boundary pass;
  *   QSIM_SWAP_LOWBIT          fused, low-bit swap schedule (QSIM_LOWSWAP=1, G = 2);
  *   QSIM_SWAP_COLLECTIVE      out of place through the transport's grouped send/recv;
- *   QSIM_SWAP_INPLACE_STAGED  in place through a bounded staging ring (no second buffer). */
+ *   QSIM_SWAP_INPLACE_STAGED  in place through a bounded staging ring (no second buffer;
+ *                             QSIM_FUSED_SWAP=0);
+ *   QSIM_SWAP_FUSED_INPLACE   no second buffer (the n = 36 shape): the passes of a layer store the
+ *                             swapped amplitudes into the peers' current buffers, each tile after
+ *                             its partner tile on the peer has been loaded (per-tile handshake
+ *                             flags over NVLink).
+ * The default is the fused split swap when a second shard buffer fits on every rank with 8 GiB to
+ * spare, else the fused in-place swap; QSIM_SWAP_INPLACE=1 forces the no-second-buffer paths. */
 enum { QSIM_SWAP_NONE = 0, QSIM_SWAP_FUSED_SPLIT = 1, QSIM_SWAP_FUSED = 2, QSIM_SWAP_LOWBIT = 3,
-       QSIM_SWAP_COLLECTIVE = 4, QSIM_SWAP_INPLACE_STAGED = 5 };
+       QSIM_SWAP_COLLECTIVE = 4, QSIM_SWAP_INPLACE_STAGED = 5, QSIM_SWAP_FUSED_INPLACE = 6 };
 int qsim_swap_path(const qsim_t *q);
 
 /* Number of qubits of the handle (QSIM_EINVAL for NULL). */

@@ -75,6 +75,22 @@ struct PassParams {
     // [mv_lo, mv_hi) move, the others are written out of place locally)
     int wsh;
     unsigned mv_lo, mv_hi;
+    // in-place fused swap (multi-GPU without a second shard buffer, the n = 36 path): a moving
+    // pass stores its peer-bound amplitudes into the peers' CURRENT buffers, in place.  The
+    // partner of a moving tile (the tile its data replaces) sits at the same visiting slot s on
+    // the peer: the boundary pass (mv 2) visits the same tile ids on every rank; mv-1 passes visit
+    // tile id (slot tile) ^ (rank << xor_cp) (xor_cp = tile-id position of the swapped bits).
+    // Handshake per slot: after its tile's TMA load has landed, rank c writes epoch into
+    // fl_peer[d][c * fl_stride + s] of every destination d; a rank stores into rank c's slot-s
+    // tile only after seeing fl_own[c * fl_stride + s] >= epoch (release / acquire, system scope).
+    // A wait longer than ~20 s sets *err (mapped host word) and gives up (no GPU hang).
+    int ip;
+    unsigned epoch;
+    int xor_cp;
+    u64 fl_stride;
+    unsigned *fl_own;
+    unsigned *fl_peer[8];
+    int *err;
     // tile visiting order: the CTA's k-th tile is rotl(k, ord_rot) over ord_bits tile-id bits,
     // so that the tiles in flight at one time span all groups (moving passes interleave NVLink
     // and HBM traffic instead of alternating phases of each); 0 = natural order

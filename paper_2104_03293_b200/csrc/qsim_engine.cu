@@ -347,6 +347,14 @@ struct qsim {
     int cur = 0;                       // which of bufs[] currently holds the state
     double2 *bufs[2] = {nullptr, nullptr};
     double2 *peer[2][8] = {};          // peer[b][c] = rank c's buffer b (own buffer for c == rank)
+    // in-place fused swap (no second buffer; PassParams::ip): peer[0][c] = rank c's state, the
+    // per-slot handshake flags (world x tiles u32 per rank) and a mapped host error word
+    bool ipfused = false;
+    unsigned epoch = 0;
+    unsigned *d_flags = nullptr;
+    unsigned *fl_peer[8] = {};
+    int *h_err = nullptr, *d_err = nullptr;
+    int grid_cap = 0;                  // moving passes' grid (loopback ranks sharing one device)
     cudaStream_t st = nullptr;
     bool own_stream = false;
     qc::Comm *comm = nullptr;          // cross-rank transport (NCCL + CUDA IPC, or the loopback)
@@ -404,6 +412,14 @@ int fail(qsim *q, int code, const std::string &msg) {
 #define CM(call)                                                                              \
     do {                                                                                      \
         if (!(call)) return fail(q, QSIM_ENCCL, std::string(#call) + ": " + q->comm->error()); \
+    } while (0)
+
+// stream sync that also reports a timed-out in-place swap handshake (PassParams::err)
+#define SYNC(q)                                                                                      \
+    do {                                                                                             \
+        CK(cudaStreamSynchronize((q)->st));                                                          \
+        if ((q)->h_err && *(q)->h_err)                                                               \
+            return fail(q, QSIM_ECUDA, "in-place swap handshake timed out (a rank stopped?)");       \
     } while (0)
 
 int grid_for(const qsim *q, u64 ntiles) {
@@ -537,7 +553,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 
 // launch one pass: TMA-pipelined kernel (one CTA per SM)
 // `out`: output buffer of an out-of-place pass (TMA stores go there), nullptr = in place
-int launch_pass(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, double2 *out = nullptr) {
+int launch_pass(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, double2 *out = nullptr,
+                int grid_max = 0) {
     if (P.kind == qk::K_TURN_RUN && P.gmix == 0 && !P.f32 && P.multi != 2) {
         // pattern factors of the phase frame (W: register bits = tile bits 3..7), the same sums
         // as err_of<FW> over the current physical frame of J
@@ -572,7 +589,7 @@ int launch_pass(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, dou
             P.tm_clen[d] = S.tm_clen[d];
             P.tm_cshift[d] = S.tm_cshift[d];
         }
-        int grid = (int)std::min<u64>((u64)q->num_sms, S.ntiles);
+        int grid = (int)std::min<u64>((u64)(grid_max > 0 ? grid_max : q->num_sms), S.ntiles);
         CK(qk::launch_tma_pass(tm[0], out ? tm[1] : tm[0], P, grid, q->st));
         *grid_out = grid;
     }
@@ -601,9 +618,11 @@ void swap_bookkeeping(qsim *q) {
 // relabelling takes effect
 int finish_fused_swap(qsim *q, bool done) {
     CM(q->comm->barrier(q->st));
-    q->cur ^= 1;
-    q->psi = q->bufs[q->cur];
-    q->tmp = q->bufs[q->cur ^ 1];
+    if (!q->ipfused) {  // out of place: the other buffer now holds the state
+        q->cur ^= 1;
+        q->psi = q->bufs[q->cur];
+        q->tmp = q->bufs[q->cur ^ 1];
+    }
     if (done) swap_bookkeeping(q);
     return QSIM_OK;
 }
@@ -837,8 +856,22 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
                     P.ord_rot = tpos % P.ord_bits;
                 }
             }
-            for (int c = 0; c < q->world; ++c) P.dst[c] = q->peer[q->cur ^ 1][c];
-            outbuf = q->bufs[q->cur ^ 1];
+            if (q->ipfused) {  // in place: the peers' current buffers, after the per-slot handshake
+                for (int c = 0; c < q->world; ++c) {
+                    P.dst[c] = q->peer[0][c];
+                    P.fl_peer[c] = q->fl_peer[c];
+                }
+                P.ip = 1;
+                P.epoch = ++q->epoch;
+                P.fl_own = q->d_flags;
+                P.fl_stride = S.ntiles;
+                P.err = q->d_err;
+                const int cb = q->m - q->g;  // tile-id position of the swapped (top local) bits
+                P.xor_cp = cb - __builtin_popcountll(S.lmask & ((1ull << cb) - 1ull));
+            } else {
+                for (int c = 0; c < q->world; ++c) P.dst[c] = q->peer[q->cur ^ 1][c];
+                outbuf = q->bufs[q->cur ^ 1];
+            }
             if (op.mv == 1 && P.mv_pbits > 0) {
                 // visit the tiles group bits first (the group bits are tile-id bits of every
                 // non-boundary set; their tile-id position = non-tile bits below them)
@@ -859,7 +892,7 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
             CK(cudaEventRecord(e0, q->st));
         }
         {
-            int rc = launch_pass(q, S, P, &grid, outbuf);
+            int rc = launch_pass(q, S, P, &grid, outbuf, op.mv && q->ipfused ? q->grid_cap : 0);
             if (rc) return rc;
         }
         if (q->prof) {
@@ -960,7 +993,7 @@ int gather_host(qsim *q, u64 first, u64 count, const uint64_t *hlist, double *ou
         q->launches++;
         if (q->world > 1) CM(q->comm->allreduce((double *)dout, c * 2, qc::Op::Sum, q->st));
         CK(cudaMemcpyAsync(out + 2 * done, dout, c * sizeof(double2), cudaMemcpyDeviceToHost, q->st));
-        CK(cudaStreamSynchronize(q->st));
+        SYNC(q);
     }
     return QSIM_OK;
 }
@@ -1073,6 +1106,35 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
             for (int b = 0; b < 2 && fuse; ++b)
                 for (int c = 0; c < world; ++c) q->peer[b][c] = (double2 *)mp[b][c];
         }
+        // in-place fused swap: no second buffer (the n = 36 shape), peer stores into the peers'
+        // current buffers after a per-slot handshake (PassParams::ip).  QSIM_FUSED_SWAP=0 keeps
+        // the staged collective swap instead.
+        if (!fuse && !q->tmp && !q->user_buf && q->m > qk::KT && !(fz && std::atoi(fz) == 0)) {
+            const u64 nt = 1ull << (q->m - qk::KT);
+            void *mp[8] = {}, *fp[8] = {};
+            CK(cudaMalloc(&q->d_flags, sizeof(unsigned) * nt * world));
+            CK(cudaMemsetAsync(q->d_flags, 0, sizeof(unsigned) * nt * world, q->st));
+            CK(cudaHostAlloc(&q->h_err, sizeof(int), cudaHostAllocMapped));
+            *q->h_err = 0;
+            CK(cudaHostGetDevicePointer(&q->d_err, q->h_err, 0));
+            CK(cudaStreamSynchronize(q->st));
+            bool ok = q->comm->share(q->psi, bytes, mp, q->st);
+            if (ok && !q->comm->share(q->d_flags, sizeof(unsigned) * nt * world, fp, q->st)) {
+                q->comm->unshare(mp);
+                ok = false;
+            }
+            if (ok) {
+                for (int c = 0; c < world; ++c) {
+                    q->peer[0][c] = (double2 *)mp[c];
+                    q->fl_peer[c] = (unsigned *)fp[c];
+                }
+                q->bufs[0] = q->psi;
+                q->ipfused = fuse = true;
+                // loopback ranks on one device: the moving passes of all ranks must be resident
+                // at once (they wait on each other's loads), so each takes 1/world of the SMs
+                if (!std::strcmp(q->comm->kind(), "loopback")) q->grid_cap = std::max(1, q->num_sms / world);
+            }
+        }
         if (fuse) {
             q->fused_swap = true;
             q->cur = 0;
@@ -1096,7 +1158,7 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
             // element (STG).  An earlier kernel made the boundary pass's STG stores cost ~1.7 ms
             // whatever its share, so G = 2 used "0,1,1" -- no longer the better choice (below).
             {
-                q->lowswap = lowswap_layout(q->m, q->g) && q->sets.size() >= 3;
+                q->lowswap = !q->ipfused && lowswap_layout(q->m, q->g) && q->sets.size() >= 3;
             }
             // (re-measured with the final pass kernels: equal shares are best at G = 2 too,
             // 20.7-20.9 vs 22.5 ms per layer with "0,1,1"; profiles/r1_mgpu2_split_weights.jsonl)
@@ -1157,9 +1219,12 @@ int qsim_destroy(qsim_t *q) {
         if (q->comm) {  // no rank may unmap while a peer could still write into it
             q->comm->barrier(q->st);
             cudaStreamSynchronize(q->st);
-            for (int b = 0; b < 2; ++b) q->comm->unshare(reinterpret_cast<void **>(q->peer[b]));
+            for (int b = 0; b < (q->ipfused ? 1 : 2); ++b) q->comm->unshare(reinterpret_cast<void **>(q->peer[b]));
+            if (q->ipfused) q->comm->unshare(reinterpret_cast<void **>(q->fl_peer));
         }
     }
+    if (q->d_flags) cudaFree(q->d_flags);
+    if (q->h_err) cudaFreeHost(q->h_err);
     delete q->comm;
     if (q->psi && q->psi != q->user_buf) cudaFree(q->psi);
     if (q->tmp && q->tmp != q->user_buf) cudaFree(q->tmp);
@@ -1351,7 +1416,7 @@ int qsim_expect_hc(qsim_t *q, double *out) {
     if (rc) return rc;
     double r[2];
     CK(cudaMemcpyAsync(r, q->d_res, sizeof(r), cudaMemcpyDeviceToHost, q->st));
-    CK(cudaStreamSynchronize(q->st));
+    SYNC(q);
     *out = r[0];
     return QSIM_OK;
 }
@@ -1364,7 +1429,7 @@ int qsim_norm2(qsim_t *q, double *out) {
     if (rc) return rc;
     double r[2];
     CK(cudaMemcpyAsync(r, q->d_res, sizeof(r), cudaMemcpyDeviceToHost, q->st));
-    CK(cudaStreamSynchronize(q->st));
+    SYNC(q);
     *out = r[1];
     return QSIM_OK;
 }
@@ -1424,7 +1489,7 @@ int qsim_energies(qsim_t *q, uint64_t first, uint64_t count, double *out) {
         q->launches++;
         if (q->world > 1) CM(q->comm->allreduce((double *)q->d_scratch, c, qc::Op::Sum, q->st));
         CK(cudaMemcpyAsync(out + done, q->d_scratch, c * sizeof(double), cudaMemcpyDeviceToHost, q->st));
-        CK(cudaStreamSynchronize(q->st));
+        SYNC(q);
     }
     return QSIM_OK;
 }
@@ -1460,7 +1525,7 @@ int qsim_spin_expectations(qsim_t *q, double *out) {
     if (q->world > 1) CM(q->comm->allreduce(vec, q->n, qc::Op::Sum, q->st));
     std::vector<double> phys(q->n);
     CK(cudaMemcpyAsync(phys.data(), vec, sizeof(double) * q->n, cudaMemcpyDeviceToHost, q->st));
-    CK(cudaStreamSynchronize(q->st));
+    SYNC(q);
     for (int a = 0; a < q->n; ++a) out[a] = phys[q->pos[a]];  // flips already folded in
     return QSIM_OK;
 }
@@ -1613,7 +1678,7 @@ int qsim_enumerate(int n, const double *h, const double *J, uint64_t *out, int m
 
 int qsim_sync(qsim_t *q) {
     if (!q) return QSIM_EINVAL;
-    CK(cudaStreamSynchronize(q->st));
+    SYNC(q);
     return QSIM_OK;
 }
 
@@ -1749,6 +1814,7 @@ int qsim_num_qubits(const qsim_t *q) { return q ? q->n : QSIM_EINVAL; }
 int qsim_swap_path(const qsim_t *q) {
     if (!q) return QSIM_EINVAL;
     if (q->world == 1) return QSIM_SWAP_NONE;
+    if (q->ipfused) return QSIM_SWAP_FUSED_INPLACE;
     if (q->fused_swap) return q->lowswap ? QSIM_SWAP_LOWBIT : (q->split ? QSIM_SWAP_FUSED_SPLIT : QSIM_SWAP_FUSED);
     return q->tmp ? QSIM_SWAP_COLLECTIVE : QSIM_SWAP_INPLACE_STAGED;
 }

@@ -117,12 +117,66 @@ struct TmaIssue {
     volatile int *issued;  // tiles issued into each stage so far
 };
 
-// tile id of the CTA's k-th tile (PassParams::ord_rot; multi-GPU moving passes only)
+// tile id of the CTA's k-th tile (PassParams::ord_rot, ::xor_cp; multi-GPU moving passes only)
 template <int MV>
 __device__ __forceinline__ u64 tile_of(const PassParams &P, u64 k) {
-    if (!MV || !P.ord_rot) return k;
-    const u64 mask = (1ull << P.ord_bits) - 1ull;
-    return ((k << P.ord_rot) | (k >> (P.ord_bits - P.ord_rot))) & mask;
+    if (!MV) return k;
+    u64 u = k;
+    if (P.ord_rot) {
+        const u64 mask = (1ull << P.ord_bits) - 1ull;
+        u = ((k << P.ord_rot) | (k >> (P.ord_bits - P.ord_rot))) & mask;
+    }
+    if (P.ip && P.mv == 1) u ^= (u64)P.rank << P.xor_cp;
+    return u;
+}
+
+// ---- in-place fused swap handshake (PassParams::ip)
+__device__ __forceinline__ void ip_signal(const PassParams &P, int dest, u64 slot) {
+    unsigned *f = P.fl_peer[dest] + (u64)P.rank * P.fl_stride + slot;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(P.epoch) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void ip_wait(const PassParams &P, int src, u64 slot) {
+    const unsigned *f = P.fl_own + (u64)src * P.fl_stride + slot;
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if ((int)(v - P.epoch) >= 0) return;
+    const uint64_t t0 = globaltimer_ns();
+    for (unsigned k = 0;; ++k) {
+        __nanosleep(128);
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if ((int)(v - P.epoch) >= 0) return;
+        if ((k & 1023u) == 1023u && globaltimer_ns() - t0 > 20000000000ull) {
+            atomicExch_system(P.err, 1);
+            return;
+        }
+    }
+}
+// the tile of slot s was loaded: tell the ranks that will store into it
+__device__ __forceinline__ void ip_signal_tile(const PassParams &P, u64 tb, u64 slot) {
+    if (P.mv == 2) {
+        for (int c = 0; c < (1 << P.gbits); ++c)
+            if (c != P.rank) ip_signal(P, c, slot);
+    } else if (P.mv == 1) {
+        const int sh = P.m - P.gbits;
+        const unsigned vr = (unsigned)((tb >> sh) & ((1ull << P.gbits) - 1ull));
+        const unsigned pr = (unsigned)((tb >> P.mv_pshift) & ((1ull << P.mv_pbits) - 1ull));
+        if (vr != (unsigned)P.rank && pr >= P.mv_lo && pr < P.mv_hi) ip_signal(P, (int)vr, slot);
+    }
+}
+// before storing into the peers' slot-s tiles: wait for their loads (one thread, then the group)
+__device__ __forceinline__ void ip_wait_peers(const PassParams &P, int gt, int g, u64 slot, int only = -1) {
+    if (gt == 0) {
+        if (only >= 0) ip_wait(P, only, slot);
+        else
+            for (int c = 0; c < (1 << P.gbits); ++c)
+                if (c != P.rank) ip_wait(P, c, slot);
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(128) : "memory");
 }
 
 // global sequence index of the CTA's i-th tile (cyclic over CTAs)
@@ -313,6 +367,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         V *sm = reinterpret_cast<V *>(stages + (size_t)s * SM_TILE_BYTES);
         const TileRec *R = srec + s;
         if (load_state || need_e) wait_tile(I, i);
+        if (MV && P.ip && gt == 0) ip_signal_tile(P, tb, seq_of(P, i));
         // ------------------------------------------------ compact turning-run body
         // (instruction-cache footprint: one copy of the butterflies, the smem sweeps and the
         // phase, driven by four mix steps X(mix1) W(mix1) [phase] W(mix2) X(mix2))
@@ -373,8 +428,10 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                     if (gt == 0 && i + NSTAGE < ntl) issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
                 }
                 store_lowswap<FX>(v, P, tb + offX, 0);
-            } else if (MV && P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
-            else if (P.tma_store) {
+            } else if (MV && P.swap_store) {
+                if (P.ip) ip_wait_peers(P, gt, g, seq_of(P, i));
+                store_tile_swapped<FX>(v, P, tb + offX);
+            } else if (P.tma_store) {
                 sts_frame<FX>(v, sm, lane, warp);
                 fence_async_smem();
                 group_bar(g);
@@ -447,8 +504,10 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         // ------------------------------------------------ finish in registers, store
         if (TURN) {
             MIXF(FX, P.mix2 & TMX, 2);
-            if (MV && P.swap_store) store_tile_swapped<FX>(v, P, tb + offX);
-            else if (tstore) {
+            if (MV && P.swap_store) {
+                if (P.ip) ip_wait_peers(P, gt, g, seq_of(P, i));
+                store_tile_swapped<FX>(v, P, tb + offX);
+            } else if (tstore) {
                 sts_frame<FX>(v, sm, lane, warp);
                 fence_async_smem();
                 group_bar(g);
@@ -498,6 +557,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                         if (gt == 0 && i + NSTAGE < ntl)
                             issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
                     }
+                    if (P.ip) ip_wait_peers(P, gt, g, seq_of(P, i), (int)vr);
                     const u64 wm = ((1ull << P.gbits) - 1ull) << sh;
                     store_tile<RUN ? FRN : FZ>(v, reinterpret_cast<V *>(P.dst[vr]) + ((tb & ~wm) | ((u64)P.rank << sh)) + offS,
                                               P.L, skE);

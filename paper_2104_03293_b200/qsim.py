@@ -28,7 +28,7 @@ QSIM_ENCCL = -7
 QSIM_FP64 = 0
 QSIM_FP32 = 1
 QSIM_SWAP_NONE, QSIM_SWAP_FUSED_SPLIT, QSIM_SWAP_FUSED, QSIM_SWAP_LOWBIT = 0, 1, 2, 3
-QSIM_SWAP_COLLECTIVE, QSIM_SWAP_INPLACE_STAGED = 4, 5
+QSIM_SWAP_COLLECTIVE, QSIM_SWAP_INPLACE_STAGED, QSIM_SWAP_FUSED_INPLACE = 4, 5, 6
 
 _ERRNAMES = {QSIM_EINVAL: "EINVAL", QSIM_ENOMEM: "ENOMEM", QSIM_ERANGE: "ERANGE",
              QSIM_ESTATE: "ESTATE", QSIM_EUNSUPPORTED: "EUNSUPPORTED", QSIM_ECUDA: "ECUDA",

@@ -94,7 +94,16 @@ def test_loopback_collective_swap(world, n, monkeypatch):
 def test_loopback_inplace_staged_swap(world, n, monkeypatch):
     Q = _q()
     monkeypatch.setenv("QSIM_SWAP_INPLACE", "1")
+    monkeypatch.setenv("QSIM_FUSED_SWAP", "0")
     _check(world, n, Q.QSIM_SWAP_INPLACE_STAGED, extras=(n == 24))
+
+
+@pytest.mark.parametrize("world,n", [(2, 18), (2, 24), (4, 20), (4, 24), (8, 22)])
+def test_loopback_fused_inplace_swap(world, n, monkeypatch):
+    """the n = 36 path (no second buffer): peer stores in place after the per-tile handshake"""
+    Q = _q()
+    monkeypatch.setenv("QSIM_SWAP_INPLACE", "1")
+    _check(world, n, Q.QSIM_SWAP_FUSED_INPLACE, extras=(n == 24))
 
 
 @pytest.mark.parametrize("n", [23, 24])
@@ -110,14 +119,17 @@ def test_loopback_split_weights(monkeypatch):
     _check(2, 24, Q.QSIM_SWAP_FUSED_SPLIT, extras=False)
 
 
-@pytest.mark.parametrize("world,n", [(2, 31), (4, 32)])
-def test_loopback_full_size_structured(world, n):
+@pytest.mark.parametrize("world,n,inplace", [(2, 31, 0), (4, 32, 0), (2, 32, 1), (4, 33, 1)])
+def test_loopback_full_size_structured(world, n, inplace, monkeypatch):
     """the bench's per-GPU shard (2^30 amplitudes per rank) on the fused split path: p = 1
     closed-form <H_C>, energies, cluster (P9) and product (P8) amplitudes spanning global bits"""
     import torch
 
-    need = world * 2 * 16 * (1 << (n - (world.bit_length() - 1))) + (8 << 30)
+    need = world * (1 if inplace else 2) * 16 * (1 << (n - (world.bit_length() - 1))) + (8 << 30)
     if torch.cuda.mem_get_info()[0] < need:
         pytest.skip("not enough device memory for the loopback shards")
     Q = _q()
-    _check(world, n, Q.QSIM_SWAP_FUSED_SPLIT, p=3, full=False, extras=False)
+    if inplace:
+        monkeypatch.setenv("QSIM_SWAP_INPLACE", "1")
+    _check(world, n, Q.QSIM_SWAP_FUSED_INPLACE if inplace else Q.QSIM_SWAP_FUSED_SPLIT, p=3, full=False,
+           extras=False)
