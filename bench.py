@@ -127,6 +127,39 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
+class NvlinkCounters:
+    """NVLink data throughput counters of one GPU (NVML field values, KiB since driver load,
+    summed over links): bytes actually sent / received over NVLink during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def read(self):
+        if not self.ok:
+            return None
+        try:
+            nv = self.nv
+            vals = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                                        nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
+            out = []
+            for v in vals:
+                if v.nvmlReturn != 0:
+                    return None
+                out.append(float(v.value.ullVal) * 1024.0)
+            return out
+        except Exception:
+            return None
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -419,6 +452,8 @@ def main():
     barrier()
     clk = ClockSampler(local)
     clk.start()
+    nvl = NvlinkCounters(local) if world > 1 else None
+    nvl0 = nvl.read() if nvl else None
     launches0 = sim.launches
     Q.qsim_profile_enable(sim.h, True)
     barrier()
@@ -430,6 +465,7 @@ def main():
     ev1.record(stream)
     barrier()
     ms = ev0.elapsed_time(ev1)
+    nvl1 = nvl.read() if nvl else None
     pass_list, pass_kinds = Q.qsim_profile_passes(sim.h, cap=1 << 16, kinds=True)
     Q.qsim_profile_enable(sim.h, False)
     pass_ms = float(np.sum(pass_list))
@@ -461,6 +497,7 @@ def main():
     h2d = h_host.nbytes + J_host.nbytes + 3 * w["s"].nbytes + 8
     d2h = 16 + 16
 
+    swap_path = sim.swap_path
     peak, peak_src = peaks()
     m = args.nlocal
     per_kind = pass_roofline(pass_list, pass_kinds, m, es, peak)
@@ -523,7 +560,14 @@ def main():
                         "peak_GBps_per_dir": 770.0,
                         "peak_source": "B200_PROFILING.md measured peer copy (nominal 900)",
                         "note": "one global-qubit swap per layer, its stores spread over the layer's passes "
-                                "(split swap); implied rate = swap bytes / whole layer time"}
+                                "(split swap); implied rate = swap bytes / whole layer time",
+                        "swap_path": swap_path,
+                        "nvml_counters_rank0": ({"tx_bytes": nvl1[0] - nvl0[0], "rx_bytes": nvl1[1] - nvl0[1],
+                                                 "tx_GBps": (nvl1[0] - nvl0[0]) / (ms / 1e3) / 1e9,
+                                                 "rx_GBps": (nvl1[1] - nvl0[1]) / (ms / 1e3) / 1e9,
+                                                 "tx_bytes_per_layer": (nvl1[0] - nvl0[0]) / (args.steps * p),
+                                                 "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX over the timed region"}
+                                                if nvl0 and nvl1 else None)}
                        if world > 1 else None),
             "clocks": clocks,
             "results": {"expect_hc": e, "expect_hc_plus_C": e + w["C"], "p_success": ps, "r": w["r"],

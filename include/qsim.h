@@ -77,11 +77,14 @@ int qsim_create(int n, int precision, qsim_t **out);
  * communicator, so use a fresh id per handle.  Two kinds:
  *   - an ncclUniqueId from qsim_nccl_unique_id (rank 0 creates it and broadcasts the bytes):
  *     one process per GPU, NCCL over NVLink, peer buffers mapped with CUDA IPC;
- *   - a loopback id from qsim_loopback_id (test transport): the `world` ranks are threads of
- *     ONE process on the current device, each creating its handle with the same id and
- *     driving it from its own thread (every call is still a collective).  Each rank owns its
- *     shard buffers and stream; collectives are stream-ordered with CUDA events and a host
- *     barrier; the pass kernels store into the peers' buffers exactly as over NVLink.
+ *   - a loopback id from qsim_loopback_id: the `world` ranks are threads of ONE process, each
+ *     creating its handle with the same id on its thread's current device and driving it from
+ *     its own thread (every call is still a collective).  All ranks on one device = the one-GPU
+ *     test mode of every multi-GPU swap path; one device per rank = a single-process multi-GPU
+ *     run (peer access enabled between the devices; e.g. for ncu, which cannot follow a
+ *     multi-process NCCL job).  Each rank owns its shard buffers and stream; collectives are
+ *     stream-ordered with CUDA events and a host barrier; the pass kernels store into the
+ *     peers' buffers exactly as over NVLink with IPC mappings.
  * `state_buf` (device pointer, optional) provides caller-owned storage of buf_bytes >= 16 *
  * 2^(n-g) bytes (the library then does not allocate the state); `cuda_stream` (cudaStream_t,
  * optional) is the stream all work is enqueued on.  world must be a power of two <= 8 with

@@ -157,6 +157,7 @@ struct LoopGroup {
     std::vector<const void *> ptr;
     std::vector<long long> val;
     std::vector<cudaEvent_t> ev;
+    std::vector<int> dev;  // each rank's device
     int attached = 0, detached = 0;
 };
 
@@ -178,8 +179,16 @@ class LoopComm final : public Comm {
             err_ = "cudaEventCreate";
             return false;
         }
+        int d = 0;
+        cudaGetDevice(&d);
         std::lock_guard<std::mutex> lk(g_->mu);
         g_->ev[rank_] = ev_;
+        g_->dev[rank_] = d;
+        return true;
+    }
+    bool shared_device() const override {
+        for (int r = 1; r < g_->world; ++r)
+            if (g_->dev[r] != g_->dev[0]) return false;
         return true;
     }
     int rank() const override { return rank_; }
@@ -234,11 +243,26 @@ class LoopComm final : public Comm {
         }
         return barrier(st);
     }
-    bool share(void *mine, size_t, void **out, cudaStream_t) override {
+    bool share(void *mine, size_t, void **out, cudaStream_t st) override {
         g_->ptr[rank_] = mine;
         if (!host_barrier()) return false;
-        for (int r = 0; r < g_->world; ++r) out[r] = const_cast<void *>(g_->ptr[r]);
-        return host_barrier();
+        long long ok = 1;
+        for (int r = 0; r < g_->world; ++r) {
+            out[r] = const_cast<void *>(g_->ptr[r]);
+            if (g_->dev[r] != g_->dev[rank_]) {  // another GPU of this process: direct peer access
+                cudaError_t e = cudaDeviceEnablePeerAccess(g_->dev[r], 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else if (e != cudaSuccess) {
+                    cudaGetLastError();
+                    ok = 0;
+                }
+            }
+        }
+        if (!host_barrier()) return false;
+        long long all = 0;
+        if (!agree_min(ok, &all, st)) return false;
+        if (!all) err_ = "peer access between the loopback ranks' devices is not possible";
+        return all != 0;
     }
     void unshare(void **) override {}
     bool agree_min(long long v, long long *out, cudaStream_t) override {
@@ -307,6 +331,7 @@ int make_loopback_id(int world, void *out128) {
     g->ptr.assign(world, nullptr);
     g->val.assign(world, 0);
     g->ev.assign(world, nullptr);
+    g->dev.assign(world, 0);
     unsigned long long key;
     {
         std::lock_guard<std::mutex> lk(g_mu);

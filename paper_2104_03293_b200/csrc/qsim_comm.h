@@ -3,8 +3,10 @@
 //
 //   NcclComm  one process per GPU, NCCL over NVLink / NVSwitch; peer state buffers mapped with
 //             CUDA IPC (the production path, P:104-108 partitioning).
-//   LoopComm  "loopback" test transport: the G ranks are threads of ONE process on ONE device,
-//             each with its own stream and its own shard buffers.  Collectives are stream-ordered
+//   LoopComm  "loopback" transport: the G ranks are threads of ONE process, on one device (the
+//             one-GPU test mode) or one device each (a single-process multi-GPU run, e.g. for
+//             ncu, which cannot follow a multi-process NCCL job), each with its own stream and
+//             shard buffers.  Collectives are stream-ordered
 //             with CUDA events plus a host barrier; peer "mappings" are the peers' raw pointers.
 //             The engine, the pass kernels (the MV instances with their peer stores), the
 //             split-swap group ranges and the permutation / flip bookkeeping are exactly those
@@ -53,6 +55,9 @@ class Comm {
     virtual void unshare(void **mapped) = 0;
     // host-side agreement, synchronous: minimum of v over ranks
     virtual bool agree_min(long long v, long long *out, cudaStream_t st) = 0;
+    // true when every rank drives the same device (loopback on one GPU): kernels that wait on
+    // each other must then fit on the device together
+    virtual bool shared_device() const { return false; }
     const std::string &error() const { return err_; }
 
   protected:

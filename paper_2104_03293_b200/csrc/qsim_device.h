@@ -99,6 +99,7 @@ struct PassParams {
     // the host (FP64 R_x turning-run passes of the single-GPU and top-bit schedules): read from
     // the constant bank instead of shared memory
     double2 PRR[NR];
+    int pw;              // per-warp turning-run kernel (tma_turn_pw_kernel; 128B-swizzled stage)
     int dbg;             // diagnostics (qsim_bench_pass): bit 0 skip stores, bit 1 skip state loads
     int tma_store;       // store tiles with TMA from the stage instead of STG from registers
     // general mixer (QSDS combined step, NEXT-1): per tile bit a 2x2 complex matrix

@@ -556,9 +556,9 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 int launch_pass(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, double2 *out = nullptr,
                 int grid_max = 0) {
     if (P.kind == qk::K_TURN_RUN && P.gmix == 0 && !P.f32 && P.multi != 2) {
-        // pattern factors of the phase frame (W: register bits = tile bits 3..7), the same sums
-        // as err_of<FW> over the current physical frame of J
-        const int n = q->n, RB = 3;
+        // pattern factors of the phase frame (W: register bits = tile bits 3..7; A of the per-warp
+        // kernel: tile bits 7..11), the same sums as err_of<F> over the current physical frame of J
+        const int n = q->n, RB = P.pw ? 7 : 3;
         int fr = 0;
         for (int r = 0; r < 5; ++r) fr |= (int)((P.flip >> S.L[RB + r]) & 1ull) << r;
         for (int j = 0; j < qk::NR; ++j) {
@@ -580,7 +580,8 @@ int launch_pass(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, dou
         const CUtensorMapDataType dt = q->f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
         for (int k = 0; k < (out ? 2 : 1); ++k) {
             CUresult r = enc(&tm[k], dt, 5u, (void *)(k ? out : q->psi), S.tm_dim,
-                             S.tm_stride + 1, S.tm_box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             S.tm_stride + 1, S.tm_box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             P.pw ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS)
                 return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
@@ -595,6 +596,20 @@ int launch_pass(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, dou
     }
     q->launches++;
     return QSIM_OK;
+}
+
+// the per-warp turning-run kernel (tma_turn_pw_kernel): single GPU, FP64, R_x mixers, a run set
+// of 3 passengers + a 9-bit run (128-byte TMA rows, the SWIZZLE_128B box), no fused reduction.
+// QSIM_TURN_PW=0 selects the group-synchronous kernel instead (A/B measurements, tests).
+bool pw_eligible(const qsim *q, const TileSet &S, const qk::PassParams &P) {
+    const bool off = std::getenv("QSIM_TURN_PW") && std::atoi(std::getenv("QSIM_TURN_PW")) == 0;
+    if (off || q->world != 1 || q->f32 || P.gmix || P.kind != qk::K_TURN_RUN || P.reduce) return false;
+    if (S.full12 || S.own != 0xFF8u || S.tm_box[0] != 16) return false;
+    // the kernel mixes the whole run twice (mix1 empty only on the write-only init pass)
+    if (P.mix2 != S.own || !(P.mix1 == S.own || (P.mix1 == 0u && P.init))) return false;
+    for (int i = 0; i < 3; ++i)
+        if (S.L[i] != i) return false;
+    return true;
 }
 
 int finish_reduce(qsim *q, int nparts) {
@@ -836,6 +851,7 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         P.reduce = op.reduce;
         P.gamma = op.gamma;
         P.rec = q->d_rec;
+        P.pw = pw_eligible(q, S, P) ? 1 : 0;
         double2 *outbuf = nullptr;  // out-of-place output (moving passes of the fused swap)
         if (op.mv) {
             P.swap_store = op.mv == 2;
@@ -1132,7 +1148,7 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
                 q->ipfused = fuse = true;
                 // loopback ranks on one device: the moving passes of all ranks must be resident
                 // at once (they wait on each other's loads), so each takes 1/world of the SMs
-                if (!std::strcmp(q->comm->kind(), "loopback")) q->grid_cap = std::max(1, q->num_sms / world);
+                if (q->comm->shared_device()) q->grid_cap = std::max(1, q->num_sms / world);
             }
         }
         if (fuse) {
@@ -1739,6 +1755,7 @@ int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
     P.gamma = 0.1;
     P.rec = q->d_rec;
     P.flip = q->flip;
+    P.pw = pw_eligible(q, S, P) && !P.dbg ? 1 : 0;
     CK(qk::launch_tile_fields(P, q->d_rec, q->st));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));

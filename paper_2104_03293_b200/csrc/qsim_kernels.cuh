@@ -112,7 +112,10 @@ __device__ __forceinline__ double energy_direct(const double *hp, const double *
 //   W: lanes t0,t1,t2,t8,t9,  warps t10,t11, regs t3..t7    (run phase / store)
 //   V: lanes t0,t1,t7,t8,t9,  warps t10,t11, regs t2..t6    (run frame of the low-bit swap
 //      schedule, multi-GPU: the passenger t2 is mixed with the run; lane-skewed)
-enum { FX = 0, FY = 1, FZ = 2, FW = 3, FV = 4 };
+//   A: lanes t2..t6,          warps t0,t1,   regs t7..t11   (per-warp turning run, 128B-swizzled
+//   B: lanes t2,t8..t11,      warps t0,t1,   regs t3..t7     stage: tma_turn_pw_kernel; the warp
+//      bits are passengers, so A <-> B exchanges stay inside a warp; B is lane-skewed on t3,t4)
+enum { FX = 0, FY = 1, FZ = 2, FW = 3, FV = 4, FA = 5, FB = 6 };
 template <int F> struct Frame;
 template <> struct Frame<FX> {
     static constexpr int RB = 7;
@@ -137,6 +140,14 @@ template <> struct Frame<FV> {
     static constexpr int RB = 2;
     __device__ static int tthr(int lane, int warp) { return (lane & 3) | ((lane >> 2) << 7) | (warp << 10); }
 };
+template <> struct Frame<FA> {
+    static constexpr int RB = 7;
+    __device__ static int tthr(int lane, int warp) { return warp | (lane << 2); }
+};
+template <> struct Frame<FB> {
+    static constexpr int RB = 3;
+    __device__ static int tthr(int lane, int warp) { return warp | ((lane & 1) << 2) | ((lane >> 1) << 8); }
+};
 
 // Lane skew of a frame's register slots in linear shared memory (element t at t * sizeof(V)):
 // slot j of a lane holds register pattern j ^ skew.  FP64 (16 B, 8 lanes per wavefront):
@@ -145,6 +156,8 @@ template <> struct Frame<FV> {
 // Frame V (lanes t0,t1,t7,..): FP64 skews t2 by t7, FP32 skews t2,t3 by t7,t8.
 template <int F, typename V>
 __device__ __forceinline__ int frame_skew(int lane) {
+    if (F == FB) return (lane >> 1) & 3;
+    if (F == FA) return 0;
     if (F == FV) return sizeof(V) == 16 ? ((lane >> 2) & 1) : ((lane >> 2) & 3);
     if (sizeof(V) == 16) return F == FY ? (lane & 7) : 0;
     return F == FY ? (lane & 15) : (F == FW ? ((lane >> 3) & 1) : 0);

@@ -613,6 +613,137 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     }
 }
 
+// ------------------------------------------------------------------ per-warp turning-run pass
+// The single-GPU FP64 turning pass on a run set with 3 passengers (t0..t2) and a 9-bit run
+// (t3..t11): mix1 on the run, the cost phase, mix2 on the run.  The tile arrives through a
+// SWIZZLE_128B tensor map: 16-byte granule g of 128-byte row r sits at granule g ^ (r & 7), i.e.
+// element t at smem index t ^ ((t >> 3) & 7).  Warp wi (0..3) of a consumer group owns the 1024
+// amplitudes with passenger bits (t0, t1) = wi in both of its frames (Frame<FA>, Frame<FB>), so
+// its frame changes are warp-private (__syncwarp) and conflict-free (the swizzle spreads the
+// fixed t0,t1 over all banks; frame B is lane-skewed on t3,t4); the four warps meet once per tile,
+// before the TMA store.  Per tile and warp: B read, mix1 (t3..t6), B -> A, mix1 (t7..t11), phase
+// (frame A: its register patterns are lane-independent, so the 32 pattern factors come from the
+// constant bank), mix2 (t7..t11), A -> B, mix2 (t3..t6), B write.
+__device__ __forceinline__ int swz128(int t) { return t ^ ((t >> 3) & 7); }
+
+// frame B element index of slot j: t = tthr_B | ((j ^ sk) << 3), swizzled; baseB folds the lane
+// parts (tthr_B ^ sk ^ (sk << 3)), the rest is a compile-time constant per j
+__device__ __forceinline__ void lds_pwB(double2 (&v)[NR], const double2 *sm, int baseB) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) v[j] = sm[baseB ^ ((j & 7) ^ (j << 3))];
+}
+__device__ __forceinline__ void sts_pwB(const double2 (&v)[NR], double2 *sm, int baseB) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) sm[baseB ^ ((j & 7) ^ (j << 3))] = v[j];
+}
+__device__ __forceinline__ void lds_pwA(double2 (&v)[NR], const double2 *sm, int baseA) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) v[j] = sm[baseA | (j << 7)];
+}
+__device__ __forceinline__ void sts_pwA(const double2 (&v)[NR], double2 *sm, int baseA) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) sm[baseA | (j << 7)] = v[j];
+}
+
+struct PwSmem {
+    static constexpr size_t align = 1024;  // SWIZZLE_128B stages must be 1024-byte aligned
+    static constexpr size_t total = TmaSmem::total + align;
+};
+
+__global__ void __launch_bounds__(TMA_NG * 128, 1)
+    tma_turn_pw_kernel(const __grid_constant__ CUtensorMap tmap, const PassParams P) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + PwSmem::align - 1) & ~(uintptr_t)(PwSmem::align - 1));
+    unsigned char *stg = smem;
+    TileRec *srec = reinterpret_cast<TileRec *>(smem + TmaSmem::rec_off);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + TmaSmem::bar_off);
+    volatile int *issued = reinterpret_cast<volatile int *>(smem + TmaSmem::iss_off);
+    double2 *uc = reinterpret_cast<double2 *>(smem + TmaSmem::uc_off);
+
+    const int tid = threadIdx.x, g = tid >> 7, gt = tid & 127, lane = gt & 31, wi = gt >> 5;
+    const bool load_state = !P.init;
+    const u64 ntl = (P.ntiles > blockIdx.x) ? (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const TmaIssue I{&tmap, &tmap, reinterpret_cast<const TileRec *>(P.rec), stg, (uint32_t)(TILE * 16), srec,
+                     full, issued};
+    if (tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) {
+            mbar_init(&full[s], 1);
+            issued[s] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int i = 0; i < NSTAGE && (u64)i < ntl; ++i) issue_tile<0>(P, I, (u64)i, i, load_state, true);
+
+    int ft = 0;
+#pragma unroll
+    for (int i = 0; i < KT; ++i) ft |= (int)((P.flip >> P.L[i]) & 1ull) << i;
+    const int tE = Frame<FA>::tthr(lane, wi) ^ ft;
+    const int fr = (ft >> Frame<FA>::RB) & 0x1F;
+    {
+        const ThreadEnergy te = thread_energy<FA>(P.Jp, P.n, P.L, lane, wi, ft);
+        uc[5 * TMA_NG * 128 + tid] = cmul(P.scale, expmi(P.gamma * te.eTT));
+#pragma unroll
+        for (int r = 0; r < 5; ++r) uc[r * TMA_NG * 128 + tid] = expmi(P.gamma * te.w[r]);
+    }
+    const int skB = frame_skew<FB, double2>(lane);
+    const int baseA = swz128(Frame<FA>::tthr(lane, wi));
+    const int baseB = Frame<FB>::tthr(lane, wi) ^ skB ^ (skB << 3);
+    __syncthreads();
+
+    double2 v[NR];
+    long long pend = -1;  // tile whose TMA store still reads its stage (deferred refill)
+    int pend_s = 0;
+    for (u64 i = g; i < ntl; i += TMA_NG) {
+        const int s = (int)(i % NSTAGE);
+        double2 *sm = reinterpret_cast<double2 *>(stg + (size_t)s * SM_TILE_BYTES);
+        const TileRec *R = srec + s;
+        wait_tile(I, i);
+        if (load_state) {
+            lds_pwB(v, sm, baseB);
+        } else {
+#pragma unroll
+            for (int j = 0; j < NR; ++j) v[j] = make_double2(P.a0, 0.0);
+        }
+        if (gt == 0 && pend >= 0) {  // deferred refill of the group's previous stage
+            bulk_wait_read0();
+            if ((u64)pend + NSTAGE < ntl) issue_tile<0>(P, I, (u64)pend + NSTAGE, pend_s, load_state, true);
+            pend = -1;
+        }
+        if (load_state) {  // mix1 = the whole run (the engine checks), or nothing on the init pass
+            stages_c<0x0Fu>(v, RxStage{P.c1.t});
+            sts_pwB(v, sm, baseB);
+            __syncwarp();
+            lds_pwA(v, sm, baseA);
+            stages_c<0x1Fu>(v, RxStage{P.c1.t});
+        }
+        {
+            double2 uu[5];
+#pragma unroll
+            for (int r = 0; r < 5; ++r) uu[r] = uc[r * TMA_NG * 128 + tid];
+            apply_phase<FA>(v, R, tE, fr, uc[5 * TMA_NG * 128 + tid], uu, P.PRR, nullptr, 0);
+        }
+        stages_c<0x1Fu>(v, RxStage{P.c2.t});
+        sts_pwA(v, sm, baseA);
+        __syncwarp();
+        lds_pwB(v, sm, baseB);
+        stages_c<0x0Fu>(v, RxStage{P.c2.t});
+        sts_pwB(v, sm, baseB);
+        fence_async_smem();
+        group_bar(g);
+        if (gt == 0) {
+            int c[5];
+            tile_coords(P, tile_of<0>(P, seq_of(P, i)), c);
+            tma_store_5d(&tmap, c, sm);
+            pend = (long long)i;
+            pend_s = s;
+        }
+    }
+    if (pend >= 0) bulk_wait_read0();
+}
+
 size_t tma_smem_bytes() { return TmaSmem::total; }
 
 template <int GMIX, typename V, int MV>
@@ -638,7 +769,9 @@ cudaError_t setup_tma_kernels_v() {
 }
 
 cudaError_t setup_tma_kernels() {
-    cudaError_t e = setup_tma_kernels_v<double2, 0>();
+    cudaError_t e = cudaFuncSetAttribute(tma_turn_pw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)PwSmem::total);
+    if (e == cudaSuccess) e = setup_tma_kernels_v<double2, 0>();
     if (e == cudaSuccess) e = setup_tma_kernels_v<double2, 1>();
     if (e == cudaSuccess) e = setup_tma_kernels_v<double2, 2>();
     if (e == cudaSuccess) e = setup_tma_kernels_v<float2, 0>();
@@ -677,6 +810,11 @@ cudaError_t launch_tma_pass_v(const CUtensorMap &tm, const CUtensorMap &sm, cons
 // schedules, 2 = the low-bit swap schedule (run frame V)
 cudaError_t launch_tma_pass(const CUtensorMap &tm, const CUtensorMap &sm, const PassParams &P, int grid,
                             cudaStream_t s) {
+    if (P.pw) {  // tm is the SWIZZLE_128B map of the run set (in place)
+        if (P.f32 || P.multi || P.kind != K_TURN_RUN || P.gmix || P.reduce) return cudaErrorInvalidValue;
+        tma_turn_pw_kernel<<<grid, TMA_NG * 128, PwSmem::total, s>>>(tm, P);
+        return cudaGetLastError();
+    }
     if (P.f32) return P.multi == 2 ? launch_tma_pass_v<float2, 2>(tm, sm, P, grid, s)
                       : P.multi ? launch_tma_pass_v<float2, 1>(tm, sm, P, grid, s)
                                 : launch_tma_pass_v<float2, 0>(tm, sm, P, grid, s);
