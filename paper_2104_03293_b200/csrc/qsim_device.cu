@@ -179,6 +179,7 @@ template <typename V>
 __global__ void __launch_bounds__(512) small_kernel(const SmallParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *st = reinterpret_cast<double2 *>(smem_raw);  // FP64 working copy (FP32 states round on store)
+    double *et = reinterpret_cast<double *>(smem_raw + ((size_t)16 << P.n));  // E(z), once per launch
     V *psi = reinterpret_cast<V *>(P.psi);
     __shared__ double sh[KT];
     __shared__ double sJ[KT * KT];
@@ -188,9 +189,10 @@ __global__ void __launch_bounds__(512) small_kernel(const SmallParams P) {
     for (int i = tid; i < n * n; i += nt) sJ[i] = P.Jp[i];
     for (int i = tid; i < dim; i += nt) st[i] = P.init ? make_double2(P.a0, 0.0) : dcast(psi[i]);
     __syncthreads();
+    for (int z = tid; z < dim; z += nt) et[z] = energy_direct(sh, sJ, n, (u64)z);  // same sum, cached
     for (int k = 0; k < P.p; ++k) {
-        const double g = P.ang[k], b = P.ang[P.p + k];
-        for (int z = tid; z < dim; z += nt) st[z] = cmul(st[z], expmi(g * energy_direct(sh, sJ, n, (u64)z)));
+        const double g = P.ang ? P.ang[k] : P.angv[k], b = P.ang ? P.ang[P.p + k] : P.angv[P.p + k];
+        for (int z = tid; z < dim; z += nt) st[z] = cmul(st[z], expmi(g * et[z]));
         double sb, cb;
         sincos(b, &sb, &cb);
         for (int q = 0; q < n; ++q) {
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(512) small_kernel(const SmallParams P) {
         psi[z] = av;
         const double2 a = dcast(av);
         if (P.reduce) {
-            const double e = energy_direct(sh, sJ, n, (u64)z);
+            const double e = et[z];
             const double pz = fma(a.x, a.x, a.y * a.y);
             acc_e = fma(pz, e, acc_e);
             acc_n += pz;
@@ -334,9 +336,9 @@ cudaError_t setup_kernels() {
     e = cudaFuncSetAttribute(reduce_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)SmemLayout::total);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(small_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * TILE);
+    e = cudaFuncSetAttribute(small_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * TILE);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(small_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * TILE);
+    return cudaFuncSetAttribute(small_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * TILE);
 }
 
 cudaError_t launch_tile_fields(const PassParams &P, void *rec, cudaStream_t s) {
@@ -357,8 +359,8 @@ cudaError_t launch_sum_partials(const double *part, int nparts, double *res, cud
 }
 
 cudaError_t launch_small(const SmallParams &P, cudaStream_t s) {
-    if (P.f32) small_kernel<float2><<<1, 512, (size_t)16 << P.n, s>>>(P);
-    else small_kernel<double2><<<1, 512, (size_t)16 << P.n, s>>>(P);
+    if (P.f32) small_kernel<float2><<<1, 512, (size_t)24 << P.n, s>>>(P);
+    else small_kernel<double2><<<1, 512, (size_t)24 << P.n, s>>>(P);
     return cudaGetLastError();
 }
 

@@ -114,12 +114,14 @@ struct SmallParams {
     int f32;             // FP32 state (float2 *) instead of FP64
     double2 *psi;
     const double *hp, *Jp;
-    const double *ang;   // gamma[p], beta[p]
+    const double *ang;   // gamma[p], beta[p] in device memory, or nullptr: in angv (p <= SMALL_PMAX)
     const double2 *gmat; // optional general mixers: [p][n][4] (then beta is unused)
     int n, p, init, reduce;
     double a0;
     double *res;         // 2 doubles
+    double angv[2 * 64]; // the angles by value (no host copy, no sync: the n = 12 grid scans)
 };
+constexpr int SMALL_PMAX = 64;
 
 struct GatherParams {
     int n, m;

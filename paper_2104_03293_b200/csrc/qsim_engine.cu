@@ -728,22 +728,29 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         if (rc) return rc;
     }
     if (q->m <= qk::KT) {  // whole state in one CTA (single GPU only)
-        if ((size_t)2 * p > q->ang_cap) {
-            if (q->d_ang) cudaFree(q->d_ang);
-            q->d_ang = nullptr;
-            CK(cudaMalloc(&q->d_ang, sizeof(double) * 2 * p));
-            q->ang_cap = 2 * p;
-        }
+        qk::SmallParams S{};
         std::vector<double> ang(2 * p);
         std::copy(gam, gam + p, ang.begin());
         std::copy(bet, bet + p, ang.begin() + p);
-        CK(cudaMemcpyAsync(q->d_ang, ang.data(), sizeof(double) * 2 * p, cudaMemcpyHostToDevice, q->st));
-        qk::SmallParams S{};
+        bool sync = q->gmats != nullptr;  // host buffers that the async copies read
+        if (p <= qk::SMALL_PMAX) {  // angles by value: no copy, no sync
+            std::copy(ang.begin(), ang.end(), S.angv);
+            S.ang = nullptr;
+        } else {
+            if ((size_t)2 * p > q->ang_cap) {
+                if (q->d_ang) cudaFree(q->d_ang);
+                q->d_ang = nullptr;
+                CK(cudaMalloc(&q->d_ang, sizeof(double) * 2 * p));
+                q->ang_cap = 2 * p;
+            }
+            CK(cudaMemcpyAsync(q->d_ang, ang.data(), sizeof(double) * 2 * p, cudaMemcpyHostToDevice, q->st));
+            S.ang = q->d_ang;
+            sync = true;
+        }
         S.f32 = q->f32;
         S.psi = q->psi;
         S.hp = q->cur_hp;
         S.Jp = q->cur_Jp;
-        S.ang = q->d_ang;
         S.n = q->n;
         S.p = p;
         S.init = q->pending_plus ? 1 : 0;
@@ -760,8 +767,7 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         S.res = q->d_res;
         CK(qk::launch_small(S, q->st));
         q->launches++;
-        // the host copy of the angles must outlive the async copy
-        CK(cudaStreamSynchronize(q->st));
+        if (sync) CK(cudaStreamSynchronize(q->st));  // the host copies must outlive the async copies
         q->pending_plus = false;
         q->res_valid = !q->gmats;
         return QSIM_OK;
