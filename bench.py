@@ -133,6 +133,8 @@ class NvlinkCounters:
 
     def __init__(self, gpu_index: int):
         self.ok = False
+        self.err = None
+        self.idx = gpu_index
         try:
             import pynvml
 
@@ -140,24 +142,37 @@ class NvlinkCounters:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
             self.ok = True
-        except Exception:
-            self.ok = False
+        except Exception as e:
+            self.err = f"nvmlInit: {e!r}"
 
     def read(self):
-        if not self.ok:
-            return None
+        if self.ok:
+            try:
+                nv = self.nv
+                vals = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                                            nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
+                out = []
+                for v in vals:
+                    if v.nvmlReturn != 0:
+                        raise RuntimeError(f"field value return {v.nvmlReturn}")
+                    out.append(float(v.value.ullVal) * 1024.0)
+                return out
+            except Exception as e:
+                self.err = f"nvml field values: {e!r}"
+        # fallback: nvidia-smi nvlink -gt d (per-link data counters in KiB)
         try:
-            nv = self.nv
-            vals = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
-                                                        nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
-            out = []
-            for v in vals:
-                if v.nvmlReturn != 0:
-                    return None
-                out.append(float(v.value.ullVal) * 1024.0)
-            return out
-        except Exception:
-            return None
+            txt = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(self.idx)], capture_output=True,
+                                 text=True, timeout=20).stdout
+            import re
+
+            tx = sum(int(x) for x in re.findall(r"Data Tx:\s*(\d+)\s*KiB", txt))
+            rx = sum(int(x) for x in re.findall(r"Data Rx:\s*(\d+)\s*KiB", txt))
+            if tx or rx:
+                return [tx * 1024.0, rx * 1024.0]
+            self.err = (self.err or "") + " | nvidia-smi nvlink: " + txt[:300].replace("\n", " / ")
+        except Exception as e:
+            self.err = (self.err or "") + f" | nvidia-smi nvlink: {e!r}"
+        return None
 
 
 def peaks():
@@ -566,8 +581,9 @@ def main():
                                                  "tx_GBps": (nvl1[0] - nvl0[0]) / (ms / 1e3) / 1e9,
                                                  "rx_GBps": (nvl1[1] - nvl0[1]) / (ms / 1e3) / 1e9,
                                                  "tx_bytes_per_layer": (nvl1[0] - nvl0[0]) / (args.steps * p),
-                                                 "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX over the timed region"}
-                                                if nvl0 and nvl1 else None)}
+                                                 "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX (or nvidia-smi nvlink "
+                                                          "-gt d) over the timed region"}
+                                                if nvl0 and nvl1 else {"unavailable": nvl.err if nvl else None})}
                        if world > 1 else None),
             "clocks": clocks,
             "results": {"expect_hc": e, "expect_hc_plus_C": e + w["C"], "p_success": ps, "r": w["r"],

@@ -161,3 +161,24 @@ def test_plan_low_bit_swap(Q, monkeypatch):
         assert passes == 2 * p + 1 and swaps == p and amps * 2 == 1 << 30
     monkeypatch.delenv("QSIM_LOWSWAP")
     assert Q.qsim_plan_positions(n, 2, 1)[29] == 30  # default: top local bit <-> global
+
+
+def test_loopback_ids(Q):
+    """qsim_loopback_id: host-only group ids (magic prefix + key + world), fresh per call; worlds
+    other than 1, 2, 4, 8 are EINVAL.  A loopback id is not mistaken for an ncclUniqueId."""
+    a, b = Q.qsim_loopback_id(2), Q.qsim_loopback_id(2)
+    assert len(a) == 128 and a != b and a[:15] == b"QSIM-LOOPBACK-1" == b[:15]
+    assert int.from_bytes(a[24:28], "little") == 2
+    for w in (0, 3, 16):
+        with pytest.raises(Q.QsimError) as ei:
+            Q.qsim_loopback_id(w)
+        assert ei.value.code == Q.QSIM_EINVAL
+
+
+def test_profile_pass_codes_match_header(Q):
+    txt = open(HEADER).read()
+    for name in ("QSIM_PASS_PLAIN12", "QSIM_PASS_PLAIN_RUN", "QSIM_PASS_TURN12", "QSIM_PASS_TURN_RUN",
+                 "QSIM_PASS_MOVING", "QSIM_PASS_INIT", "QSIM_PASS_REDUCE", "QSIM_SWAP_FUSED_INPLACE",
+                 "QSIM_SWAP_INPLACE_STAGED", "QSIM_SWAP_COLLECTIVE", "QSIM_SWAP_LOWBIT", "QSIM_SWAP_FUSED_SPLIT"):
+        m = re.search(name + r"\s*=\s*(\d+)", txt)
+        assert m and int(m.group(1)) == getattr(Q, name), name
