@@ -1183,9 +1183,13 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
                 q->lowswap = !q->ipfused && lowswap_layout(q->m, q->g) && q->sets.size() >= 3;
             }
             // (re-measured with the final pass kernels: equal shares are best at G = 2 too,
-            // 20.7-20.9 vs 22.5 ms per layer with "0,1,1"; profiles/r1_mgpu2_split_weights.jsonl)
+            // 20.7-20.9 vs 22.5 ms per layer with "0,1,1"; profiles/r1_mgpu2_split_weights.jsonl).
+            // With four or more sets (m >= 31) the boundary pass moves nothing: a moving boundary
+            // pass stores every element from registers (no TMA store), which cost ~20 ms of its
+            // ~51 at n = 34 (in place, 2 B200s: 219 ms per layer with equal shares, 204 with
+            // "0,1,1,1"; profiles/r2_mgpu2_split_weights.jsonl)
             q->split_w.clear();
-            q->split_w.push_back(1.0);
+            q->split_w.push_back(q->sets.size() >= 4 ? 0.0 : 1.0);
             for (int s2 = (int)q->sets.size() - 2; s2 >= 0; --s2) q->split_w.push_back(1.0);
             if (const char *w = std::getenv("QSIM_SPLIT_W")) {
                 std::vector<double> ws;
