@@ -29,6 +29,6 @@ with Q.QSim(a.n) as sim:
     sim.set_ising(h, J)
     for _ in range(a.reps):
         sim.init_plus()
-        sim.apply_aqa(0.4 * a.p, a.p, s, 2 * np.pi * A, 2 * np.pi * B / r)
+        sim.apply_aqa(0.02 * a.p, a.p, s, 2 * np.pi * A, 2 * np.pi * B / r)
         e = sim.expect_hc()
     print("expect_hc", e, "launches", sim.launches)

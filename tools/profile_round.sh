@@ -10,6 +10,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT
     $BENCH > "$OUT/ncu_launches.log" 2>&1
 PROF="python tools/prof_run.py --n 30 --p 4"
 $PROF > "$OUT/prof_plain.log" 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:tma_pass_kernel -s 1 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:tma_ -s 1 -c 3 \
     -o "$OUT/tma_pass_full" $PROF > "$OUT/ncu_full.log" 2>&1
 echo done

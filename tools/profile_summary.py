@@ -20,13 +20,13 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ap = argparse.ArgumentParser()
 ap.add_argument("dir")
-ap.add_argument("--tag", default="r1")
+ap.add_argument("--tag", default="r2")
 a = ap.parse_args()
 prof = os.path.join(ROOT, "profiles")
 
 
 def short(name):
-    name = re.sub(r"\((CUtensorMap|PassParams|const|double|unsigned|float|int \*).*$", "", name)
+    name = re.sub(r"\((CUtensorMap|PassParams|const|double|unsigned|float|int \*|qk::).*$", "", name)
     return name.replace("qk::", "").replace("void ", "")
 
 
@@ -50,7 +50,7 @@ tot = sum(t for _, t in agg.values())
 out = [f"# {a.tag}: ncu launch list of `python bench.py --steps 1 --warmup 3 --no-cpu-baseline` (n=30, p=32, 1 B200)",
        "# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised: compare SHARES)",
        "# tma_pass_kernel<KIND, MIXER, amplitude type, 1gpu|mgpu>: KIND 0 = 12-bit set plain, 1 = run plain,",
-       "#   3 = run turning (phase); MIXER 0 = R_x",
+       "#   3 = run turning (phase); MIXER 0 = R_x; tma_turn_pw_kernel = the per-warp turning-run pass",
        f"{'kernel':60s} {'launches':>8s} {'total ms':>10s} {'share':>7s} {'avg us':>10s}"]
 for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     out.append(f"{k:60s} {c:8d} {t:10.2f} {100 * t / tot:6.1f}% {1e3 * t / c:10.1f}")
@@ -94,14 +94,28 @@ for r in body:
     })
 for x in launches:  # achieved DRAM rate (cold-cache, under ncu: context for the live bench figure)
     x["dram_GBps"] = (x["dram_read_GB"] + x["dram_write_GB"]) / (x["duration_ms"] / 1e3)
-turn = [x for x in launches if "<3," in x["kernel"]]
-pick = turn[0] if turn else launches[0]
-dram = (pick["dram_read_GB"] + pick["dram_write_GB"]) * 1e9
+def program(k):
+    if "tma_turn_pw_kernel" in k or "<3," in k:
+        return "turning run"
+    return {"<0,": "12-bit plain", "<1,": "plain run", "<2,": "12-bit turning"}.get(
+        next((t for t in ("<0,", "<1,", "<2,") if t in k), ""), "other")
+
+
 alg = 32.0 * 2 ** 30
-js = {"kernel": f"{short(pick['kernel'])} (the turning pass; largest share of the bench step: {dominant})",
+per = {}
+for x in launches:
+    pr = program(x["kernel"])
+    dram = (x["dram_read_GB"] + x["dram_write_GB"]) * 1e9
+    if pr not in per:
+        per[pr] = {"kernel": short(x["kernel"]), "dram_bytes_per_launch": dram, "algorithmic_bytes_per_launch": alg,
+                   "traffic_over_algorithmic": dram / alg, "duration_ms": x["duration_ms"],
+                   "fp64_pipe_pct": x["fp64_pipe_pct"], "lsu_shared_wavefronts_pct": x["lsu_shared_wavefronts_pct"]}
+pick = per.get("turning run") or next(iter(per.values()))
+js = {"source": f"profiles/{a.tag}_tma_pass_full_raw.csv (ncu --set full --clock-control none, tools/prof_run.py --n 30 --p 4)",
+      "kernel": f"{pick['kernel']} (the turning pass; largest share of the bench step: {dominant})",
       "config": "n=30 (2^30 amplitudes), tools/prof_run.py --n 30 --p 4, ncu --set full --clock-control none",
-      "dram_bytes_per_launch": dram, "algorithmic_bytes_per_launch": alg, "traffic_over_algorithmic": dram / alg,
-      "launches": launches}
+      "dram_bytes_per_launch": pick["dram_bytes_per_launch"], "algorithmic_bytes_per_launch": alg,
+      "traffic_over_algorithmic": pick["traffic_over_algorithmic"], "per_program": per, "launches": launches}
 json.dump(js, open(os.path.join(prof, "pass_kernel_traffic.json"), "w"), indent=1)
 print(json.dumps({k: v for k, v in js.items() if k != "launches"}, indent=1))
 for x in launches:
