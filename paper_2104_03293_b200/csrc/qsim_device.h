@@ -84,6 +84,11 @@ struct PassParams {
     // fl_peer[d][c * fl_stride + s] of every destination d; a rank stores into rank c's slot-s
     // tile only after seeing fl_own[c * fl_stride + s] >= epoch (release / acquire, system scope).
     // A wait longer than ~20 s sets *err (mapped host word) and gives up (no GPU hang).
+    // whole-tile moves (mv 1) with TMA tensor stores: dmaps[c] = tensor map of the set's view of
+    // rank c's destination buffer (device memory, 128 B each); chunk_cp = tile-id position of the
+    // swapped bits (a moving tile u lands at tile id u with those bits = rank); nullptr = STG
+    const ::CUtensorMap_st *dmaps;
+    int chunk_cp;
     int ip;
     unsigned epoch;
     int xor_cp;

@@ -355,6 +355,8 @@ struct qsim {
     unsigned *fl_peer[8] = {};
     int *h_err = nullptr, *d_err = nullptr;
     int grid_cap = 0;                  // moving passes' grid (loopback ranks sharing one device)
+    void *d_maps = nullptr;            // per-destination tensor maps of the whole-tile moving passes
+    int tma_moves = 1;                 // QSIM_TMA_MOVES=0: whole-tile moves as STG from registers
     cudaStream_t st = nullptr;
     bool own_stream = false;
     qc::Comm *comm = nullptr;          // cross-rank transport (NCCL + CUDA IPC, or the loopback)
@@ -610,6 +612,29 @@ bool pw_eligible(const qsim *q, const TileSet &S, const qk::PassParams &P) {
     for (int i = 0; i < 3; ++i)
         if (S.L[i] != i) return false;
     return true;
+}
+
+// tensor maps of set S over every rank's destination buffer of a whole-tile moving pass
+// (P.dst[c]), copied stream-ordered into q->d_maps (the previous pass's kernel has finished with
+// them by then); the kernel stores a moving tile with the map of its destination rank
+int encode_dest_maps(qsim *q, const TileSet &S, qk::PassParams &P) {
+    auto enc = tmap_encoder();
+    if (!enc) return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    if (!q->d_maps) CK(cudaMalloc(&q->d_maps, sizeof(CUtensorMap) * 8));
+    CUtensorMap maps[8];
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    const CUtensorMapDataType dt = q->f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+    for (int c = 0; c < q->world; ++c) {
+        CUresult r = enc(&maps[c], dt, 5u, (void *)P.dst[c], S.tm_dim, S.tm_stride + 1, S.tm_box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled (peer) failed: " + std::to_string((int)r));
+    }
+    CK(cudaMemcpyAsync(q->d_maps, maps, sizeof(CUtensorMap) * q->world, cudaMemcpyHostToDevice, q->st));
+    P.dmaps = reinterpret_cast<const CUtensorMap_st *>(q->d_maps);
+    const int cb = q->m - q->g;
+    P.chunk_cp = cb - __builtin_popcountll(S.lmask & ((1ull << cb) - 1ull));
+    return QSIM_OK;
 }
 
 int finish_reduce(qsim *q, int nparts) {
@@ -893,6 +918,11 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
             } else {
                 for (int c = 0; c < q->world; ++c) P.dst[c] = q->peer[q->cur ^ 1][c];
                 outbuf = q->bufs[q->cur ^ 1];
+            }
+            if (op.mv == 1 && q->tma_moves && P.tma_store) {
+                // TMA tensor stores of the moving tiles: one map per destination buffer
+                int rc = encode_dest_maps(q, S, P);
+                if (rc) return rc;
             }
             if (op.mv == 1 && P.mv_pbits > 0) {
                 // visit the tiles group bits first (the group bits are tile-id bits of every
@@ -1207,6 +1237,7 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     }
     q->pending_plus = true;
     if (const char *e = std::getenv("QSIM_TMA_STORE")) q->tma_store = std::atoi(e) != 0;
+    if (const char *e = std::getenv("QSIM_TMA_MOVES")) q->tma_moves = std::atoi(e) != 0;
     CK(qk::setup_tma_kernels());
     for (const TileSet &S : q->sets)
         if (!S.tm_ok) return fail(q, QSIM_EUNSUPPORTED, "tile set without a 5-D TMA view");
@@ -1250,6 +1281,7 @@ int qsim_destroy(qsim_t *q) {
         }
     }
     if (q->d_flags) cudaFree(q->d_flags);
+    if (q->d_maps) cudaFree(q->d_maps);
     if (q->h_err) cudaFreeHost(q->h_err);
     delete q->comm;
     if (q->psi && q->psi != q->user_buf) cudaFree(q->psi);

@@ -555,6 +555,24 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 const unsigned vr = (unsigned)((tb >> sh) & ((1ull << P.gbits) - 1ull));
                 const unsigned pr = (unsigned)((tb >> P.mv_pshift) & ((1ull << P.mv_pbits) - 1ull));
                 if (vr != (unsigned)P.rank && pr >= P.mv_lo && pr < P.mv_hi) {
+                    if (P.dmaps && tstore) {  // TMA tensor store of the whole tile into rank vr's buffer
+                        sts_frame<RUN ? FRN : FZ>(v, sm, lane, warp);
+                        fence_async_smem();
+                        group_bar(g);
+                        if (gt == 0) {
+                            if (P.ip) {
+                                ip_wait(P, (int)vr, seq_of(P, i));
+                                asm volatile("fence.proxy.async.global;" ::: "memory");
+                            }
+                            const u64 cm = ((1ull << P.gbits) - 1ull) << P.chunk_cp;
+                            int c[5];
+                            tile_coords(P, (ut & ~cm) | ((u64)P.rank << P.chunk_cp), c);
+                            tma_store_5d(reinterpret_cast<const CUtensorMap *>(P.dmaps) + vr, c, sm);
+                            pend = (long long)i;
+                            pend_s = s;
+                        }
+                        continue;
+                    }
                     if (late_release) {
                         fence_async_smem();
                         group_bar(g);

@@ -82,3 +82,6 @@ def test_n33_energies_sampled(big33):
     assert np.array_equal(big33.energies(first, 5000), o.energies(h, J, first, 5000))
     z_star = int(sum(int(x_star[i]) << i for i in range(N)))
     assert big33.energies(z_star, 1)[0] + C == 0.0
+    # P10's 10^7 labels at n = 33: a contiguous block at a seeded offset (one gather, one oracle call)
+    first = int(inst.sample_indices(N, 4, seed=21)[1]) % ((1 << N) - 10_000_000)
+    assert np.array_equal(big33.energies(first, 10_000_000), o.energies(h, J, first, 10_000_000))

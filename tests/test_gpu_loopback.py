@@ -1,11 +1,12 @@
 """Multi-GPU swap paths on ONE GPU: the G ranks
 of a sharded handle are threads of this process (the loopback transport of qsim_loopback_id),
 each with its own shard buffers and stream.  The engine, the pass kernels with their peer
-stores, the split-swap group ranges and the permutation / flip bookkeeping are the NCCL path's;
-only the transport differs.  Every swap path runs here: fused split (default), collective
-(QSIM_FUSED_SWAP=0), in-place staged (QSIM_SWAP_INPLACE=1, the n = 36 path), low-bit
-(QSIM_LOWSWAP=1) and non-default split weights (QSIM_SPLIT_W), against the oracle (full
-state at n <= 24, structured pins P4/P8/P9 at n = 31, 32)."""
+stores, the split-swap group ranges, the in-place handshake and the permutation / flip
+bookkeeping are the NCCL path's; only the transport differs.  Every swap path runs here: fused
+split (default), fused in place (QSIM_SWAP_INPLACE=1: no second buffer, the n = 36 path),
+collective (QSIM_FUSED_SWAP=0), staged in place (both), low-bit (QSIM_LOWSWAP=1) and
+non-default split weights (QSIM_SPLIT_W), against the oracle (full state at n <= 24, structured
+pins P4/P8/P9 at n = 31-33, up to 8 ranks)."""
 from __future__ import annotations
 
 import threading
@@ -119,7 +120,7 @@ def test_loopback_split_weights(monkeypatch):
     _check(2, 24, Q.QSIM_SWAP_FUSED_SPLIT, extras=False)
 
 
-@pytest.mark.parametrize("world,n,inplace", [(2, 31, 0), (4, 32, 0), (2, 32, 1), (4, 33, 1)])
+@pytest.mark.parametrize("world,n,inplace", [(2, 31, 0), (4, 32, 0), (2, 32, 1), (4, 33, 1), (8, 33, 1)])
 def test_loopback_full_size_structured(world, n, inplace, monkeypatch):
     """the bench's per-GPU shard (2^30 amplitudes per rank) on the fused split path: p = 1
     closed-form <H_C>, energies, cluster (P9) and product (P8) amplitudes spanning global bits"""
@@ -133,3 +134,14 @@ def test_loopback_full_size_structured(world, n, inplace, monkeypatch):
         monkeypatch.setenv("QSIM_SWAP_INPLACE", "1")
     _check(world, n, Q.QSIM_SWAP_FUSED_INPLACE if inplace else Q.QSIM_SWAP_FUSED_SPLIT, p=3, full=False,
            extras=False)
+
+
+@pytest.mark.parametrize("world,n,inplace", [(2, 20, 0), (4, 22, 1)])
+def test_loopback_stg_moves(world, n, inplace, monkeypatch):
+    """QSIM_TMA_MOVES=0: the whole-tile moves of the split swap as 16-byte stores from registers
+    instead of TMA tensor stores through the destination ranks' tensor maps"""
+    Q = _q()
+    monkeypatch.setenv("QSIM_TMA_MOVES", "0")
+    if inplace:
+        monkeypatch.setenv("QSIM_SWAP_INPLACE", "1")
+    _check(world, n, Q.QSIM_SWAP_FUSED_INPLACE if inplace else Q.QSIM_SWAP_FUSED_SPLIT, extras=False)

@@ -298,6 +298,45 @@ def test_full_size_energies_sampled(Q, big30):
     assert big30.energies(z_star, 1)[0] + C == 0.0
 
 
+def test_full_size_energies_all_labels(Q, big30):
+    """P10 at the bench size: E(z) of every one of the 2^30 labels of the bench's exact-cover
+    instance, bit-exact against the oracle (dyadic data, reading R14), in chunks of 2^26."""
+    n = 30
+    a, _ = inst.exact_cover(n, seed=0)
+    h, J, C = op.exact_cover_to_ising(a)
+    big30.set_ising(h, J)
+    CH = 1 << 26
+    for first in range(0, 1 << n, CH):
+        assert np.array_equal(big30.energies(first, CH), o.energies(h, J, first, CH)), first
+
+
+@pytest.mark.parametrize("env", [{"QSIM_TURN_PW": "0"}, {"QSIM_RUNSPLIT": "0"}])
+def test_full_size_kernel_switches(Q, env, monkeypatch):
+    """The documented switches of the single-GPU n = 30 path: QSIM_TURN_PW=0 runs the turning
+    passes on the group-synchronous kernel instead of the per-warp one, QSIM_RUNSPLIT=0 uses
+    contiguous runs instead of the split-run layout; both against the p = 1 closed form (P4)
+    and the product-state amplitudes (P8) at p = 3."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    n = 30
+    h, J = inst.random_ising(n, 77)
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        s.init_plus()
+        s.apply_qaoa([0.37], [-0.52])
+        e = s.expect_hc()
+        ref = cf.p1_expect_hc(h, J, 0.37, -0.52)
+        assert abs(e - ref) <= 1e-9 * max(abs(ref), 1.0), (e, ref)
+        hp, Jp = inst.product_ising(n, 9)
+        g, b = rand_angles(3, 88)
+        s.set_ising(hp, Jp)
+        s.init_plus()
+        s.apply_qaoa(g, b)
+        zs = inst.sample_indices(n, 48, seed=8)
+        got = np.array([s.amplitudes(int(z), 1)[0] for z in zs])
+    assert np.max(np.abs(got - cf.product_amplitudes(hp, g, b, zs))) <= AMP_TOL
+
+
 # ------------------------------------------------------------------ NEXT-2: <sigma^z_i>
 @pytest.mark.parametrize("n,p", [(5, 3), (16, 3), (22, 2)])
 def test_spin_expectations(Q, n, p):

@@ -4,7 +4,7 @@
 set -u
 OUT=${1:-gpurun_out/prof}
 mkdir -p "$OUT"
-BENCH="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
+BENCH="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-extras"
 $BENCH > "$OUT/bench_plain.log" 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches_bench.csv" \
     $BENCH > "$OUT/ncu_launches.log" 2>&1

@@ -47,7 +47,7 @@ for r in rows:
     c, t = agg.get(k, (0, 0.0))
     agg[k] = (c + 1, t + ms)
 tot = sum(t for _, t in agg.values())
-out = [f"# {a.tag}: ncu launch list of `python bench.py --steps 1 --warmup 3 --no-cpu-baseline` (n=30, p=32, 1 B200)",
+out = [f"# {a.tag}: ncu launch list of `python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-extras` (n=30, p=32, 1 B200)",
        "# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised: compare SHARES)",
        "# tma_pass_kernel<KIND, MIXER, amplitude type, 1gpu|mgpu>: KIND 0 = 12-bit set plain, 1 = run plain,",
        "#   3 = run turning (phase); MIXER 0 = R_x; tma_turn_pw_kernel = the per-warp turning-run pass",
