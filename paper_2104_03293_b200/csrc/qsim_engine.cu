@@ -1238,6 +1238,7 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     q->pending_plus = true;
     if (const char *e = std::getenv("QSIM_TMA_STORE")) q->tma_store = std::atoi(e) != 0;
     if (const char *e = std::getenv("QSIM_TMA_MOVES")) q->tma_moves = std::atoi(e) != 0;
+
     CK(qk::setup_tma_kernels());
     for (const TileSet &S : q->sets)
         if (!S.tm_ok) return fail(q, QSIM_EUNSUPPORTED, "tile set without a 5-D TMA view");
