@@ -1105,7 +1105,9 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
         // One GPU only: on 2 and 4 GPUs the split layout (top set {12..15, 25..29}, swap groups
         // on bits 12..15) made the 12-bit pass's share of the swap slower (G = 2: 22.8 vs 22.5 ms
         // per layer, G = 4: 24.4-27.9 vs 21.7), so the multi-GPU schedules keep contiguous runs.
-        if (split_a > 0 && split_a <= 6 && world == 1 && q->sets.size() == 3 && q->m == qk::KT + 18) {
+        // (an explicit QSIM_RUNSPLIT=a applies it on any world, for measurements)
+        const bool rs_forced = std::getenv("QSIM_RUNSPLIT") && std::atoi(std::getenv("QSIM_RUNSPLIT")) > 0;
+        if (split_a > 0 && split_a <= 6 && (world == 1 || rs_forced) && q->sets.size() == 3 && q->m == qk::KT + 18) {
             const int a = split_a;
             std::vector<int> L1, L2;
             for (int i = 0; i < 3; ++i) { L1.push_back(i); L2.push_back(i); }
