@@ -78,7 +78,7 @@ def _check(world, n, expect_path, p=3, full=True, extras=True):
     assert len(out) >= 5
 
 
-@pytest.mark.parametrize("world,n", [(2, 18), (2, 24), (4, 20), (4, 24)])
+@pytest.mark.parametrize("world,n", [(2, 18), (2, 24), (4, 20), (4, 24), (8, 22)])
 def test_loopback_fused_split(world, n):
     Q = _q()
     _check(world, n, Q.QSIM_SWAP_FUSED_SPLIT)
@@ -120,7 +120,8 @@ def test_loopback_split_weights(monkeypatch):
     _check(2, 24, Q.QSIM_SWAP_FUSED_SPLIT, extras=False)
 
 
-@pytest.mark.parametrize("world,n,inplace", [(2, 31, 0), (4, 32, 0), (2, 32, 1), (4, 33, 1), (8, 33, 1)])
+@pytest.mark.parametrize("world,n,inplace", [(2, 31, 0), (4, 32, 0), (8, 32, 0), (2, 32, 1), (4, 33, 1),
+                                              (8, 33, 1)])
 def test_loopback_full_size_structured(world, n, inplace, monkeypatch):
     """the bench's per-GPU shard (2^30 amplitudes per rank) on the fused split path: p = 1
     closed-form <H_C>, energies, cluster (P9) and product (P8) amplitudes spanning global bits"""
