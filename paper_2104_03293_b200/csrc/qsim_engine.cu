@@ -357,7 +357,6 @@ struct qsim {
     int grid_cap = 0;                  // moving passes' grid (loopback ranks sharing one device)
     void *d_maps = nullptr;            // per-destination tensor maps of the whole-tile moving passes
     int tma_moves = 1;                 // QSIM_TMA_MOVES=0: whole-tile moves as STG from registers
-    int pw_mode = 1;                   // per-warp turning kernel: 1 TMA store, 2 register stores (QSIM_PW_STG=1)
     cudaStream_t st = nullptr;
     bool own_stream = false;
     qc::Comm *comm = nullptr;          // cross-rank transport (NCCL + CUDA IPC, or the loopback)
@@ -883,7 +882,7 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         P.reduce = op.reduce;
         P.gamma = op.gamma;
         P.rec = q->d_rec;
-        P.pw = pw_eligible(q, S, P) ? q->pw_mode : 0;
+        P.pw = pw_eligible(q, S, P) ? 1 : 0;
         double2 *outbuf = nullptr;  // out-of-place output (moving passes of the fused swap)
         if (op.mv) {
             P.swap_store = op.mv == 2;
@@ -1241,7 +1240,7 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     q->pending_plus = true;
     if (const char *e = std::getenv("QSIM_TMA_STORE")) q->tma_store = std::atoi(e) != 0;
     if (const char *e = std::getenv("QSIM_TMA_MOVES")) q->tma_moves = std::atoi(e) != 0;
-    if (const char *e = std::getenv("QSIM_PW_STG")) q->pw_mode = std::atoi(e) == 1 ? 2 : 1;
+
 
     CK(qk::setup_tma_kernels());
     for (const TileSet &S : q->sets)
@@ -1802,7 +1801,7 @@ int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
     P.gamma = 0.1;
     P.rec = q->d_rec;
     P.flip = q->flip;
-    P.pw = pw_eligible(q, S, P) && !P.dbg ? q->pw_mode : 0;
+    P.pw = pw_eligible(q, S, P) && !P.dbg ? 1 : 0;
     CK(qk::launch_tile_fields(P, q->d_rec, q->st));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));

@@ -714,8 +714,6 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     const int skB = frame_skew<FB, double2>(lane);
     const int baseA = swz128(Frame<FA>::tthr(lane, wi));
     const int baseB = Frame<FB>::tthr(lane, wi) ^ skB ^ (skB << 3);
-    const int baseX = swz128(Frame<FX>::tthr(lane, wi));  // frame X in the swizzled stage (pw == 2)
-    const u64 offX = thread_offset<FX>(P.L, lane, wi);
     __syncthreads();
 
     double2 v[NR];
@@ -759,20 +757,8 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         lds_pwB(v, sm, baseB);
         stages_c<0x0Fu>(v, RxStage{P.c2.t});
         sts_pwB(v, sm, baseB);
-        if (P.pw == 2) {
-            // register-store variant: the group re-reads the tile in frame X (lanes t0..t4:
-            // 128-byte rows), releases the stage at once (no wait for a TMA store's smem read)
-            // and stores from registers
-            group_bar(g);
-#pragma unroll
-            for (int j = 0; j < NR; ++j) v[j] = sm[baseX | (j << 7)];
-            fence_async_smem();
-            group_bar(g);
-            if (gt == 0 && i + NSTAGE < ntl) issue_tile<0>(P, I, i + NSTAGE, s, load_state, true);
-            store_tile<FX>(v, reinterpret_cast<double2 *>(P.psi) + tile_base(P, tile_of<0>(P, seq_of(P, i))) + offX,
-                           P.L);
-            continue;
-        }
+        // (re-reading the tile in frame X, releasing the stage at once and storing from registers
+        // was measured slower: 6.5 -> 7.0-7.2 ms)
         fence_async_smem();
         group_bar(g);
         if (gt == 0) {
