@@ -275,6 +275,7 @@ __global__ void gather_kernel(const GatherParams G, const V *psi, double2 *out) 
     for (u64 k = blockIdx.x * (u64)blockDim.x + threadIdx.x; k < G.count; k += (u64)gridDim.x * blockDim.x) {
         const u64 z = G.list ? G.list[k] : G.first + k;
         const u64 x = logical_to_physical(z, G) ^ G.flip;
+        QSIM_DCHECK((x >> G.n) == 0);
         out[k] = ((x >> G.m) == G.rank) ? dcast(psi[x & ((1ull << G.m) - 1ull)]) : make_double2(0.0, 0.0);
     }
 }
@@ -310,6 +311,7 @@ __global__ void energy_dump_kernel(const GatherParams G, const PassParams P, dou
         constexpr int RB = Frame<FZ>::RB;
         const int tthr = t & ~(0x1F << RB), j = (t >> RB) & 0x1F;
         const ThreadEnergy te = thread_energy<FZ>(P.Jp, G.n, P.L, tthr & 31, tthr >> 10, 0);
+        QSIM_DCHECK(u < P.ntiles && t < TILE);
         const TileRec &R = recs[u];
         double e = R.e[KT] + te.eTT;
 #pragma unroll

@@ -24,6 +24,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Device-side bound checks of the debug build (libqsim_debug.so, -DQSIM_DEBUG): a failed check
+// traps (cudaErrorAssert), so an out-of-range tile, address or handshake slot cannot go unseen.
+#ifdef QSIM_DEBUG
+#include <cassert>
+#define QSIM_DCHECK(c) assert(c)
+#else
+#define QSIM_DCHECK(c) ((void)0)
+#endif
+
 #include "qsim_device.h"
 
 namespace qk {

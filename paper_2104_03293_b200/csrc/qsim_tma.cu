@@ -136,6 +136,7 @@ __device__ __forceinline__ u64 tile_of(const PassParams &P, u64 k) {
 // of the thread, including its NVLink stores of the previous tiles (measured: the in-place
 // boundary pass 16.9 ms with release vs ...)
 __device__ __forceinline__ void ip_signal(const PassParams &P, int dest, u64 slot) {
+    QSIM_DCHECK(dest >= 0 && dest < (1 << P.gbits) && dest != P.rank && slot < P.fl_stride);
     unsigned *f = P.fl_peer[dest] + (u64)P.rank * P.fl_stride + slot;
     asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(f), "r"(P.epoch) : "memory");
 }
@@ -145,6 +146,7 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     return t;
 }
 __device__ __forceinline__ void ip_wait(const PassParams &P, int src, u64 slot) {
+    QSIM_DCHECK(src >= 0 && src < (1 << P.gbits) && src != P.rank && slot < P.fl_stride);
     const unsigned *f = P.fl_own + (u64)src * P.fl_stride + slot;
     unsigned v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
@@ -216,6 +218,7 @@ __device__ __forceinline__ void wait_tile(const TmaIssue &I, u64 i) {
     const int s = (int)(i % NSTAGE);
     const int need = (int)(i / NSTAGE) + 1;
     while (I.issued[s] < need) __nanosleep(32);
+    QSIM_DCHECK(I.issued[s] == need);  // the stage cannot be refilled before this tile is consumed
     mbar_wait(&I.full[s], (uint32_t)((i / NSTAGE) & 1));
 }
 
@@ -239,6 +242,7 @@ __device__ __forceinline__ void store_tile_swapped(const V (&v)[NR], const PassP
     for (int j = 0; j < NR; ++j) {
         const u64 x = xb + ((j & 1) ? s0 : 0) + ((j & 2) ? s1 : 0) + ((j & 4) ? s2 : 0) + ((j & 8) ? s3 : 0) +
                       ((j & 16) ? s4 : 0);
+        QSIM_DCHECK((x >> P.m) == 0 && (x >> sh) < (1ull << P.gbits));
         const unsigned pr = (unsigned)((x >> P.mv_pshift) & pmask);
         V *a = (pr >= P.mv_lo && pr < P.mv_hi) ? reinterpret_cast<V *>(P.dst[x >> sh]) + (rofs | (x & ymask)) : own + x;
         __stcs(a, v[j]);
@@ -368,6 +372,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         const int s = (int)(i % NSTAGE);
         const u64 ut = tile_of<MV>(P, seq_of(P, i));
         const u64 tb = tile_base(P, ut);
+        QSIM_DCHECK(ut < P.ntiles && (tb >> P.m) == 0 && (tb & P.lmask) == 0);
         V *sm = reinterpret_cast<V *>(stages + (size_t)s * SM_TILE_BYTES);
         const TileRec *R = srec + s;
         if (load_state || need_e) wait_tile(I, i);
@@ -566,6 +571,8 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                             }
                             const u64 cm = ((1ull << P.gbits) - 1ull) << P.chunk_cp;
                             int c[5];
+                            QSIM_DCHECK((((ut & ~cm) | ((u64)P.rank << P.chunk_cp)) < P.ntiles) &&
+                                        ((ut & cm) >> P.chunk_cp) == vr);
                             tile_coords(P, (ut & ~cm) | ((u64)P.rank << P.chunk_cp), c);
                             tma_store_5d(reinterpret_cast<const CUtensorMap *>(P.dmaps) + vr, c, sm);
                             pend = (long long)i;
@@ -581,6 +588,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                     }
                     if (P.ip) ip_wait_peers(P, gt, g, seq_of(P, i), (int)vr);
                     const u64 wm = ((1ull << P.gbits) - 1ull) << sh;
+                    QSIM_DCHECK(((((tb & ~wm) | ((u64)P.rank << sh)) + offS) >> P.m) == 0);
                     store_tile<RUN ? FRN : FZ>(v, reinterpret_cast<V *>(P.dst[vr]) + ((tb & ~wm) | ((u64)P.rank << sh)) + offS,
                                               P.L, skE);
                     continue;
@@ -721,6 +729,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     int pend_s = 0;
     for (u64 i = g; i < ntl; i += TMA_NG) {
         const int s = (int)(i % NSTAGE);
+        QSIM_DCHECK(tile_of<0>(P, seq_of(P, i)) < P.ntiles);
         double2 *sm = reinterpret_cast<double2 *>(stg + (size_t)s * SM_TILE_BYTES);
         const TileRec *R = srec + s;
         // (refilling the previous stage before this wait when the tile is not in yet was measured

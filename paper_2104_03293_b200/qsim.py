@@ -15,7 +15,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqsim.so")
+# QSIM_LIBRARY selects another build of the same library (the debug build libqsim_debug.so of
+# tests/test_gpu_debug_build.py); there is no fallback: the file must exist
+LIB_PATH = os.environ.get("QSIM_LIBRARY") or os.path.join(_HERE, "libqsim.so")
 
 QSIM_OK = 0
 QSIM_EINVAL = -1
