@@ -105,7 +105,10 @@ TileSet make_set(int m, const std::vector<int> &Lpos, unsigned own, int es = 16)
             if (S.tm_rank == 5) { S.tm_ok = false; break; }
             const int d = S.tm_rank;
             int take;
-            if (tile) take = std::min(len, d == 0 ? 7 : 8);
+            // a run set's passengers go in an innermost box of 3 bits (8 amplitudes = 128 bytes: the
+            // SWIZZLE_128B span of the per-warp turning kernel; the linear smem order is the same);
+            // the 12-bit set keeps 7 (1 KiB rows)
+            if (tile) take = std::min(len, d == 0 ? (own == (1u << qk::KT) - 1u ? 7 : 3) : 8);
             else take = len;
             const cuuint64_t sz = 1ull << take;
             S.tm_dim[d] = (d == 0) ? 2 * sz : sz;
@@ -600,18 +603,25 @@ int launch_pass(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, dou
     return QSIM_OK;
 }
 
-// the per-warp turning-run kernel (tma_turn_pw_kernel): single GPU, FP64, R_x mixers, a run set
-// of 3 passengers + a 9-bit run (128-byte TMA rows, the SWIZZLE_128B box), no fused reduction.
-// QSIM_TURN_PW=0 selects the group-synchronous kernel instead (A/B measurements, tests).
-bool pw_eligible(const qsim *q, const TileSet &S, const qk::PassParams &P) {
+// the per-warp turning-run kernel (tma_turn_pw_kernel): FP64, R_x mixers, a run set of 3 or 5
+// passengers (9- or 7-bit run; the passenger box is 128 bytes: the SWIZZLE_128B span), mix2 = the
+// whole run, mix1 = the whole run, nothing (init) or the top g run bits (a multi-GPU boundary
+// pass's arrivals), no fused reduction, no swap stores (any world: non-moving passes only).
+// Returns P.pw (0 = not eligible).  QSIM_TURN_PW=0 selects the group-synchronous kernel instead.
+int pw_eligible(const qsim *q, const TileSet &S, const qk::PassParams &P) {
     const bool off = std::getenv("QSIM_TURN_PW") && std::atoi(std::getenv("QSIM_TURN_PW")) == 0;
-    if (off || q->world != 1 || q->f32 || P.gmix || P.kind != qk::K_TURN_RUN || P.reduce) return false;
-    if (S.full12 || S.own != 0xFF8u || S.tm_box[0] != 16) return false;
-    // the kernel mixes the whole run twice (mix1 empty only on the write-only init pass)
-    if (P.mix2 != S.own || !(P.mix1 == S.own || (P.mix1 == 0u && P.init))) return false;
-    for (int i = 0; i < 3; ++i)
-        if (S.L[i] != i) return false;
-    return true;
+    if (off || q->f32 || P.gmix || P.kind != qk::K_TURN_RUN || P.reduce || P.mv || P.multi == 2) return 0;
+    int np = 0;
+    while (np < qk::KT && S.L[np] == np && !((S.own >> np) & 1u)) ++np;
+    if ((np != 3 && np != 5) || S.full12 || S.own != (((1u << (qk::KT - np)) - 1u) << np) || S.tm_box[0] != 16)
+        return 0;
+    if (P.mix2 != S.own) return 0;
+    int m1 = -1;
+    if (P.mix1 == S.own || (P.mix1 == 0u && P.init)) m1 = 0;
+    for (int g = 1; g <= 3 && m1 < 0; ++g)
+        if (P.mix1 == (((1u << g) - 1u) << (qk::KT - g))) m1 = g;
+    if (m1 < 0 || (m1 > 0 && np != 5)) return 0;  // arrivals-only mix1 occurs on 7-bit runs (>= 4 sets)
+    return 1 | ((np == 5) << 1) | (m1 << 2);
 }
 
 // tensor maps of set S over every rank's destination buffer of a whole-tile moving pass
@@ -882,7 +892,6 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
         P.reduce = op.reduce;
         P.gamma = op.gamma;
         P.rec = q->d_rec;
-        P.pw = pw_eligible(q, S, P) ? 1 : 0;
         double2 *outbuf = nullptr;  // out-of-place output (moving passes of the fused swap)
         if (op.mv) {
             P.swap_store = op.mv == 2;
@@ -932,6 +941,7 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
                 P.ord_rot = tpos % P.ord_bits;
             }
         }
+        P.pw = pw_eligible(q, S, P);  // after the swap setup: moving passes keep the group kernel
         if (op.phase || op.reduce) {
             CK(qk::launch_tile_fields(P, q->d_rec, q->st));
             q->launches++;
@@ -1801,7 +1811,7 @@ int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out) {
     P.gamma = 0.1;
     P.rec = q->d_rec;
     P.flip = q->flip;
-    P.pw = pw_eligible(q, S, P) && !P.dbg ? 1 : 0;
+    P.pw = P.dbg ? 0 : pw_eligible(q, S, P);
     CK(qk::launch_tile_fields(P, q->d_rec, q->st));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));

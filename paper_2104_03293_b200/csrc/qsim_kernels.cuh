@@ -124,7 +124,8 @@ __device__ __forceinline__ double energy_direct(const double *hp, const double *
 //   A: lanes t2..t6,          warps t0,t1,   regs t7..t11   (per-warp turning run, 128B-swizzled
 //   B: lanes t2,t8..t11,      warps t0,t1,   regs t3..t7     stage: tma_turn_pw_kernel; the warp
 //      bits are passengers, so A <-> B exchanges stay inside a warp; B is lane-skewed on t3,t4)
-enum { FX = 0, FY = 1, FZ = 2, FW = 3, FV = 4, FA = 5, FB = 6 };
+//   B5: lanes t2,t3,t4,t10,t11, warps t0,t1, regs t5..t9  (frame B of a 5-passenger run: no skew)
+enum { FX = 0, FY = 1, FZ = 2, FW = 3, FV = 4, FA = 5, FB = 6, FB5 = 7 };
 template <int F> struct Frame;
 template <> struct Frame<FX> {
     static constexpr int RB = 7;
@@ -156,6 +157,10 @@ template <> struct Frame<FA> {
 template <> struct Frame<FB> {
     static constexpr int RB = 3;
     __device__ static int tthr(int lane, int warp) { return warp | ((lane & 1) << 2) | ((lane >> 1) << 8); }
+};
+template <> struct Frame<FB5> {
+    static constexpr int RB = 5;
+    __device__ static int tthr(int lane, int warp) { return warp | ((lane & 7) << 2) | ((lane >> 3) << 10); }
 };
 
 // Lane skew of a frame's register slots in linear shared memory (element t at t * sizeof(V)):

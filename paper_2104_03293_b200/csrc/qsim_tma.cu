@@ -666,6 +666,16 @@ __device__ __forceinline__ void sts_pwB(const double2 (&v)[NR], double2 *sm, int
 #pragma unroll
     for (int j = 0; j < NR; ++j) sm[baseB ^ ((j & 7) ^ (j << 3))] = v[j];
 }
+// frame B5 (5 passengers): t = tthr_B5 | (j << 5); the swizzle XORs t3, t4 (lane bits, folded into
+// baseB5) and t5 = j bit 0 (compile-time per j)
+__device__ __forceinline__ void lds_pwB5(double2 (&v)[NR], const double2 *sm, int baseB5) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) v[j] = sm[baseB5 ^ ((j << 5) | ((j & 1) << 2))];
+}
+__device__ __forceinline__ void sts_pwB5(const double2 (&v)[NR], double2 *sm, int baseB5) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) sm[baseB5 ^ ((j << 5) | ((j & 1) << 2))] = v[j];
+}
 __device__ __forceinline__ void lds_pwA(double2 (&v)[NR], const double2 *sm, int baseA) {
 #pragma unroll
     for (int j = 0; j < NR; ++j) v[j] = sm[baseA | (j << 7)];
@@ -680,6 +690,26 @@ struct PwSmem {
     static constexpr size_t total = TmaSmem::total + align;
 };
 
+// NP: passengers (3: 9-bit run, frames A + B; 5: 7-bit run, frames A + B5).  M1: mix1 = the whole
+// run (0; nothing on the write-only init pass) or only the top M1 run bits (the arriving global
+// qubits of a multi-GPU boundary pass: frame A alone, one frame change fewer)
+template <int NP, int M1>
+__device__ __forceinline__ void pw_ldsB(double2 (&v)[NR], const double2 *sm, int baseB) {
+    if (NP == 3) lds_pwB(v, sm, baseB);
+    else lds_pwB5(v, sm, baseB);
+}
+template <int NP, int M1>
+__device__ __forceinline__ void pw_stsB(const double2 (&v)[NR], double2 *sm, int baseB) {
+    if (NP == 3) sts_pwB(v, sm, baseB);
+    else sts_pwB5(v, sm, baseB);
+}
+template <int NP>
+__device__ __forceinline__ void pw_mixB(double2 (&v)[NR], double t) {
+    if (NP == 3) stages_c<0x0Fu>(v, RxStage{t});  // t3..t6
+    else stages_c<0x03u>(v, RxStage{t});          // t5, t6
+}
+
+template <int NP, int M1>
 __global__ void __launch_bounds__(TMA_NG * 128, 1)
     tma_turn_pw_kernel(const __grid_constant__ CUtensorMap tmap, const PassParams P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -721,7 +751,8 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     }
     const int skB = frame_skew<FB, double2>(lane);
     const int baseA = swz128(Frame<FA>::tthr(lane, wi));
-    const int baseB = Frame<FB>::tthr(lane, wi) ^ skB ^ (skB << 3);
+    const int baseB = NP == 3 ? (Frame<FB>::tthr(lane, wi) ^ skB ^ (skB << 3))
+                              : (Frame<FB5>::tthr(lane, wi) ^ ((lane >> 1) & 3));
     __syncthreads();
 
     double2 v[NR];
@@ -736,7 +767,8 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         // slower: 6.54 -> 7.3 ms; the store's smem read completes late, so its wait stalls warp 0)
         wait_tile(I, i);
         if (load_state) {
-            lds_pwB(v, sm, baseB);
+            if (M1 == 0) pw_ldsB<NP, M1>(v, sm, baseB);
+            else lds_pwA(v, sm, baseA);
         } else {
 #pragma unroll
             for (int j = 0; j < NR; ++j) v[j] = make_double2(P.a0, 0.0);
@@ -747,12 +779,16 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             // (a TMA L2 prefetch of the tile 1-3 refills ahead was measured slower: 6.5 -> 7.4-8.3 ms)
             pend = -1;
         }
-        if (load_state) {  // mix1 = the whole run (the engine checks), or nothing on the init pass
-            stages_c<0x0Fu>(v, RxStage{P.c1.t});
-            sts_pwB(v, sm, baseB);
-            __syncwarp();
-            lds_pwA(v, sm, baseA);
-            stages_c<0x1Fu>(v, RxStage{P.c1.t});
+        if (load_state) {  // mix1 as the engine checked: the whole run, or the M1 arriving bits
+            if (M1 == 0) {
+                pw_mixB<NP>(v, P.c1.t);
+                pw_stsB<NP, M1>(v, sm, baseB);
+                __syncwarp();
+                lds_pwA(v, sm, baseA);
+                stages_c<0x1Fu>(v, RxStage{P.c1.t});
+            } else {
+                stages_c<(((1u << M1) - 1u) << (5 - M1)) & 0x1Fu>(v, RxStage{P.c1.t});
+            }
         }
         {
             double2 uu[5];
@@ -763,9 +799,9 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         stages_c<0x1Fu>(v, RxStage{P.c2.t});
         sts_pwA(v, sm, baseA);
         __syncwarp();
-        lds_pwB(v, sm, baseB);
-        stages_c<0x0Fu>(v, RxStage{P.c2.t});
-        sts_pwB(v, sm, baseB);
+        pw_ldsB<NP, M1>(v, sm, baseB);
+        pw_mixB<NP>(v, P.c2.t);
+        pw_stsB<NP, M1>(v, sm, baseB);
         // (re-reading the tile in frame X, releasing the stage at once and storing from registers
         // was measured slower: 6.5 -> 7.0-7.2 ms)
         fence_async_smem();
@@ -806,8 +842,10 @@ cudaError_t setup_tma_kernels_v() {
 }
 
 cudaError_t setup_tma_kernels() {
-    cudaError_t e = cudaFuncSetAttribute(tma_turn_pw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)PwSmem::total);
+    cudaError_t e = cudaSuccess;
+    for (auto k : {tma_turn_pw_kernel<3, 0>, tma_turn_pw_kernel<5, 0>, tma_turn_pw_kernel<5, 1>, tma_turn_pw_kernel<5, 2>,
+                   tma_turn_pw_kernel<5, 3>})
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PwSmem::total);
     if (e == cudaSuccess) e = setup_tma_kernels_v<double2, 0>();
     if (e == cudaSuccess) e = setup_tma_kernels_v<double2, 1>();
     if (e == cudaSuccess) e = setup_tma_kernels_v<double2, 2>();
@@ -847,9 +885,19 @@ cudaError_t launch_tma_pass_v(const CUtensorMap &tm, const CUtensorMap &sm, cons
 // schedules, 2 = the low-bit swap schedule (run frame V)
 cudaError_t launch_tma_pass(const CUtensorMap &tm, const CUtensorMap &sm, const PassParams &P, int grid,
                             cudaStream_t s) {
-    if (P.pw) {  // tm is the SWIZZLE_128B map of the run set (in place)
-        if (P.f32 || P.multi || P.kind != K_TURN_RUN || P.gmix || P.reduce) return cudaErrorInvalidValue;
-        tma_turn_pw_kernel<<<grid, TMA_NG * 128, PwSmem::total, s>>>(tm, P);
+    if (P.pw) {  // tm is the SWIZZLE_128B map of the run set (in place); P.pw = 1 | (NP == 5) << 1 | M1 << 2
+        if (P.f32 || P.mv || P.multi == 2 || P.kind != K_TURN_RUN || P.gmix || P.reduce) return cudaErrorInvalidValue;
+        const int np5 = (P.pw >> 1) & 1, m1 = (P.pw >> 2) & 3;
+        const size_t sh = PwSmem::total;
+        const dim3 b(TMA_NG * 128);
+        switch (np5 * 4 + m1) {
+            case 0: tma_turn_pw_kernel<3, 0><<<grid, b, sh, s>>>(tm, P); break;
+            case 4: tma_turn_pw_kernel<5, 0><<<grid, b, sh, s>>>(tm, P); break;
+            case 5: tma_turn_pw_kernel<5, 1><<<grid, b, sh, s>>>(tm, P); break;
+            case 6: tma_turn_pw_kernel<5, 2><<<grid, b, sh, s>>>(tm, P); break;
+            case 7: tma_turn_pw_kernel<5, 3><<<grid, b, sh, s>>>(tm, P); break;
+            default: return cudaErrorInvalidValue;  // 9-bit runs only occur with three sets (no arrivals-only mix1)
+        }
         return cudaGetLastError();
     }
     if (P.f32) return P.multi == 2 ? launch_tma_pass_v<float2, 2>(tm, sm, P, grid, s)

@@ -121,7 +121,7 @@ def test_loopback_split_weights(monkeypatch):
 
 
 @pytest.mark.parametrize("world,n,inplace", [(2, 31, 0), (4, 32, 0), (8, 32, 0), (2, 32, 1), (4, 33, 1),
-                                              (8, 33, 1)])
+                                              (8, 33, 1), (2, 33, 1)])
 def test_loopback_full_size_structured(world, n, inplace, monkeypatch):
     """the bench's per-GPU shard (2^30 amplitudes per rank) on the fused split path: p = 1
     closed-form <H_C>, energies, cluster (P9) and product (P8) amplitudes spanning global bits"""
