@@ -143,6 +143,13 @@ int qsim_apply_qsds(qsim_t *q, double tau, int n_steps, const double *s, const d
  * (12 gates per HBM sweep); no phase, so no qsim_set_ising is needed. */
 int qsim_apply_hadamard(qsim_t *q, int reps);
 
+/* Batched QAOA expectation values for small problems (n <= 12, one GPU): for each of the `count`
+ * angle sets b, <H_C> of |beta_b, gamma_b> (eq:QAOA_state, p layers from |+>)
+ * into out[b]; gamma, beta are [count][p] row-major host arrays.  One CTA per angle set with the
+ * whole state in shared memory -- the parameter-grid scans of the paper's Fig. 3 in one
+ * launch.  The handle's state is not touched.  QSIM_EUNSUPPORTED for n > 12 or world > 1. */
+int qsim_qaoa_batch(qsim_t *q, const double *gamma, const double *beta, int p, int count, double *out);
+
 /* Host-only helper (no device work): the angles qsim_apply_aqa uses. */
 int qsim_aqa_angles(double T, int p, const double *s, const double *A, const double *B,
                     int n_knots, double *gamma_out, double *beta_out);

@@ -256,6 +256,59 @@ __global__ void __launch_bounds__(512) small_kernel(const SmallParams P) {
     }
 }
 
+// ============================================ batched small states (grid scans, config n = 12)
+// The QAOA p = 1 landscape of P:369 (and any batch of angle sets) on a state that fits one SM:
+// CTA b evaluates point b -- |+>, p layers (phase with the launch's E table, one butterfly sweep per
+// qubit), <H_C> -- with the state in shared memory, so 2-3 points run per SM concurrently and a
+// 64 x 64 grid is one launch instead of 4096.
+__global__ void energy_table_kernel(const double *hp, const double *Jp, int n, double *etab) {
+    const int dim = 1 << n;
+    for (int z = blockIdx.x * blockDim.x + threadIdx.x; z < dim; z += gridDim.x * blockDim.x)
+        etab[z] = energy_direct(hp, Jp, n, (u64)z);
+}
+
+__global__ void __launch_bounds__(256) qaoa_batch_kernel(const BatchParams B) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int n = B.n, dim = 1 << n, tid = threadIdx.x, nt = blockDim.x;
+    double2 *st = reinterpret_cast<double2 *>(smem_raw);
+    double *et = reinterpret_cast<double *>(smem_raw + ((size_t)16 << n));
+    __shared__ double red[8];
+    for (int z = tid; z < dim; z += nt) {
+        st[z] = make_double2(B.a0, 0.0);
+        et[z] = B.etab[z];
+    }
+    __syncthreads();
+    const double *gam = B.gamma + (size_t)blockIdx.x * B.p, *bet = B.beta + (size_t)blockIdx.x * B.p;
+    for (int k = 0; k < B.p; ++k) {
+        const double g = gam[k];
+        for (int z = tid; z < dim; z += nt) st[z] = cmul(st[z], expmi(g * et[z]));
+        double sb, cb;
+        sincos(bet[k], &sb, &cb);
+        for (int q = 0; q < n; ++q) {
+            __syncthreads();
+            for (int r = tid; r < dim / 2; r += nt) {
+                const int z0 = ((r >> q) << (q + 1)) | (r & ((1 << q) - 1));
+                const int z1 = z0 | (1 << q);
+                const double2 a = st[z0], bb = st[z1];
+                st[z0] = make_double2(fma(cb, a.x, sb * bb.y), fma(cb, a.y, -sb * bb.x));
+                st[z1] = make_double2(fma(sb, a.y, cb * bb.x), fma(-sb, a.x, cb * bb.y));
+            }
+        }
+        __syncthreads();
+    }
+    double acc = 0.0;
+    for (int z = tid; z < dim; z += nt) acc = fma(fma(st[z].x, st[z].x, st[z].y * st[z].y), et[z], acc);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((tid & 31) == 0) red[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0.0;
+        for (int w = 0; w < nt / 32; ++w) a += red[w];
+        B.out[blockIdx.x] = a;
+    }
+}
+
 // ======================================================================== utilities
 template <typename V>
 __global__ void init_plus_kernel(V *psi, u64 count, double a0) {
@@ -338,6 +391,8 @@ cudaError_t setup_kernels() {
     e = cudaFuncSetAttribute(reduce_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)SmemLayout::total);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(qaoa_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * TILE);
+    if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(small_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * TILE);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(small_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * TILE);
@@ -363,6 +418,15 @@ cudaError_t launch_sum_partials(const double *part, int nparts, double *res, cud
 cudaError_t launch_small(const SmallParams &P, cudaStream_t s) {
     if (P.f32) small_kernel<float2><<<1, 512, (size_t)24 << P.n, s>>>(P);
     else small_kernel<double2><<<1, 512, (size_t)24 << P.n, s>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_qaoa_batch(const BatchParams &B, double *etab, cudaStream_t s) {
+    const int dim = 1 << B.n;
+    energy_table_kernel<<<(dim + 255) / 256, 256, 0, s>>>(B.hp, B.Jp, B.n, etab);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    qaoa_batch_kernel<<<B.count, 256, (size_t)24 << B.n, s>>>(B);
     return cudaGetLastError();
 }
 

@@ -128,6 +128,17 @@ struct SmallParams {
 };
 constexpr int SMALL_PMAX = 64;
 
+// batched small-state QAOA (qsim_qaoa_batch): one CTA per parameter point, the whole 2^n state
+// (n <= 12) in shared memory; E(z) precomputed once per launch (etab, 2^n doubles)
+struct BatchParams {
+    const double *hp, *Jp;
+    const double *gamma, *beta;  // [count][p]
+    const double *etab;          // E(z), written by the energy-table kernel of the same launch
+    double *out;                 // [count] <H_C>
+    int n, p, count;
+    double a0;
+};
+
 struct GatherParams {
     int n, m;
     u64 rank;
@@ -166,6 +177,7 @@ cudaError_t launch_tile_fields(const PassParams &P, void *rec, cudaStream_t s);
 cudaError_t launch_reduce(const PassParams &P, int grid, cudaStream_t s);
 cudaError_t launch_sum_partials(const double *part, int nparts, double *res, cudaStream_t s);
 cudaError_t launch_small(const SmallParams &P, cudaStream_t s);
+cudaError_t launch_qaoa_batch(const BatchParams &B, double *etab, cudaStream_t s);
 cudaError_t launch_init_plus(double2 *psi, u64 count, double a0, int grid, cudaStream_t s, int f32 = 0);
 cudaError_t launch_gather(const GatherParams &G, const double2 *psi, double2 *out, int grid, cudaStream_t s,
                           int f32 = 0);

@@ -1449,6 +1449,41 @@ int qsim_apply_qsds(qsim_t *q, double tau, int n_steps, const double *s, const d
     return rc;
 }
 
+int qsim_qaoa_batch(qsim_t *q, const double *gamma, const double *beta, int p, int count, double *out) {
+    if (!q) return QSIM_EINVAL;
+    if (!gamma || !beta || !out || p < 1 || count < 0) return fail(q, QSIM_EINVAL, "need gamma, beta, out, p >= 1, count >= 0");
+    if (!q->has_ising) return fail(q, QSIM_ESTATE, "qsim_set_ising not called");
+    if (q->world != 1 || q->n > qk::KT) return fail(q, QSIM_EUNSUPPORTED, "qsim_qaoa_batch needs n <= 12 on one GPU");
+    if (check_angles(gamma, p * count) || check_angles(beta, p * count)) return fail(q, QSIM_EINVAL, "angles contain NaN/Inf");
+    if (count == 0) return QSIM_OK;
+    {
+        int rc = ensure_frame(q);
+        if (rc) return rc;
+    }
+    const size_t np = (size_t)p * count, dim = (size_t)1 << q->n;
+    int rc = scratch(q, sizeof(double) * (2 * np + count + dim));
+    if (rc) return rc;
+    double *dg = (double *)q->d_scratch, *db = dg + np, *dout = db + np, *det = dout + count;
+    CK(cudaMemcpyAsync(dg, gamma, sizeof(double) * np, cudaMemcpyHostToDevice, q->st));
+    CK(cudaMemcpyAsync(db, beta, sizeof(double) * np, cudaMemcpyHostToDevice, q->st));
+    qk::BatchParams B{};
+    B.hp = q->cur_hp;
+    B.Jp = q->cur_Jp;
+    B.gamma = dg;
+    B.beta = db;
+    B.etab = det;
+    B.out = dout;
+    B.n = q->n;
+    B.p = p;
+    B.count = count;
+    B.a0 = std::pow(2.0, -0.5 * q->n);
+    CK(qk::launch_qaoa_batch(B, det, q->st));
+    q->launches += 2;
+    CK(cudaMemcpyAsync(out, dout, sizeof(double) * count, cudaMemcpyDeviceToHost, q->st));
+    SYNC(q);
+    return QSIM_OK;
+}
+
 int qsim_apply_hadamard(qsim_t *q, int reps) {
     if (!q) return QSIM_EINVAL;
     if (reps < 1) return fail(q, QSIM_EINVAL, "reps >= 1");

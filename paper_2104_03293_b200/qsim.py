@@ -38,7 +38,7 @@ _ERRNAMES = {QSIM_EINVAL: "EINVAL", QSIM_ENOMEM: "ENOMEM", QSIM_ERANGE: "ERANGE"
 
 # every symbol include/qsim.h declares (tests check the library exports all of them)
 EXPORTS = ["qsim_create", "qsim_create_ex", "qsim_destroy", "qsim_set_ising", "qsim_init_plus",
-           "qsim_apply_qaoa", "qsim_apply_aqa", "qsim_apply_qsds", "qsim_apply_hadamard", "qsim_aqa_angles", "qsim_expect_hc", "qsim_norm2",
+           "qsim_apply_qaoa", "qsim_qaoa_batch", "qsim_apply_aqa", "qsim_apply_qsds", "qsim_apply_hadamard", "qsim_aqa_angles", "qsim_expect_hc", "qsim_norm2",
            "qsim_success_prob", "qsim_get_amplitudes", "qsim_energies", "qsim_spin_expectations",
            "qsim_apply_aqa_traced", "qsim_ground_states", "qsim_enumerate", "qsim_sync",
            "qsim_plan_counts", "qsim_plan_positions", "qsim_nccl_unique_id", "qsim_loopback_id",
@@ -70,6 +70,7 @@ lib.qsim_set_ising.argtypes = [_H, _D, _D]
 lib.qsim_init_plus.argtypes = [_H]
 lib.qsim_apply_qaoa.argtypes = [_H, _D, _D, ctypes.c_int]
 lib.qsim_apply_aqa.argtypes = [_H, ctypes.c_double, ctypes.c_int, _D, _D, _D, ctypes.c_int]
+lib.qsim_qaoa_batch.argtypes = [_H, _D, _D, ctypes.c_int, ctypes.c_int, _D]
 lib.qsim_apply_qsds.argtypes = [_H, ctypes.c_double, ctypes.c_int, _D, _D, _D, ctypes.c_int]
 lib.qsim_apply_hadamard.argtypes = [_H, ctypes.c_int]
 lib.qsim_aqa_angles.argtypes = [ctypes.c_double, ctypes.c_int, _D, _D, _D, ctypes.c_int, _D, _D]
@@ -153,6 +154,19 @@ def qsim_apply_qaoa(h, gamma, beta) -> None:
     if g.shape != b.shape or g.ndim != 1:
         raise ValueError("gamma and beta must be 1-D arrays of equal length")
     _check(lib.qsim_apply_qaoa(h, _dp(g), _dp(b), int(g.shape[0])), h)
+
+
+def qsim_qaoa_batch(h, gamma, beta) -> np.ndarray:
+    """<H_C> for each row of gamma, beta ([count, p]) -- n <= 12, one launch"""
+    g, b = _f64(gamma), _f64(beta)
+    if g.ndim == 1:
+        g, b = g[:, None], b[:, None]
+    if g.shape != b.shape or g.ndim != 2:
+        raise ValueError("gamma and beta must be [count, p] arrays of equal shape")
+    g, b = np.ascontiguousarray(g), np.ascontiguousarray(b)
+    out = np.empty(g.shape[0])
+    _check(lib.qsim_qaoa_batch(h, _dp(g), _dp(b), int(g.shape[1]), int(g.shape[0]), _dp(out)), h)
+    return out
 
 
 def qsim_apply_aqa(h, T: float, p: int, s, A, B) -> None:
@@ -378,6 +392,9 @@ class QSim:
 
     def apply_qaoa(self, gamma, beta):
         qsim_apply_qaoa(self.h, gamma, beta)
+
+    def qaoa_batch(self, gamma, beta):
+        return qsim_qaoa_batch(self.h, gamma, beta)
 
     def apply_aqa(self, T, p, s, A, B):
         qsim_apply_aqa(self.h, T, p, s, A, B)

@@ -641,3 +641,36 @@ def test_energies_are_the_reducing_pass_energies(Q, n):
     assert np.max(np.abs(en - ref)) <= 1e-12 * np.max(np.abs(ref))
     p = np.abs(psi) ** 2
     assert abs(np.dot(p, en) - e_fused) <= 1e-11 * np.dot(p, np.abs(en))
+
+
+# ------------------------------------------------------------------ batched small-state QAOA (grid scans)
+@pytest.mark.parametrize("n,p,count", [(8, 1, 37), (12, 3, 65), (5, 2, 1)])
+def test_qaoa_batch_matches_oracle(Q, n, p, count):
+    """qsim_qaoa_batch: <H_C> of |beta_b, gamma_b> for every angle set b (eq:QAOA_state),
+    one CTA per set, against the oracle's state and expectation per set (reading R12 bar)."""
+    rng = np.random.default_rng(n * 100 + p)
+    if n == 12:
+        clauses, _ = inst.planted_2sat(n, seed=2)
+        h, J, C = op.two_sat_to_ising(n, clauses)
+    else:
+        h, J = inst.random_ising(n, n + 5)
+    g = rng.uniform(-2, 2, (count, p))
+    b = rng.uniform(-np.pi, np.pi, (count, p))
+    with Q.QSim(n) as s:
+        s.set_ising(h, J)
+        got = s.qaoa_batch(g, b)
+        s.init_plus()  # the batch leaves the handle's state alone
+        assert np.max(np.abs(s.amplitudes() - 2.0 ** (-n / 2))) == 0.0
+        assert s.qaoa_batch(np.zeros((0, p)), np.zeros((0, p))).shape == (0,)
+    for k in range(count):
+        psi = o.qaoa_state(h, J, g[k], b[k])
+        assert_expect_close(got[k], h, J, psi)
+
+
+def test_qaoa_batch_needs_small_state(Q):
+    with Q.QSim(13) as s:
+        h, J = inst.random_ising(13, 1)
+        s.set_ising(h, J)
+        with pytest.raises(Q.QsimError) as ei:
+            s.qaoa_batch([[0.1]], [[0.2]])
+        assert ei.value.code == Q.QSIM_EUNSUPPORTED
