@@ -255,10 +255,11 @@ enum { QSIM_PASS_PLAIN12 = 0, QSIM_PASS_PLAIN_RUN = 1, QSIM_PASS_TURN12 = 2, QSI
        QSIM_PASS_MOVING = 4, QSIM_PASS_INIT = 8, QSIM_PASS_REDUCE = 16 };
 int qsim_profile_passes(qsim_t *q, double *ms_out, int *kind_out, int cap);
 
-/* Diagnostic micro-benchmark (modifies the state): time `reps` back-to-back launches of
- * the tile pass over tile set `set` (0 = bits 0..11, 1.. = the run sets in ascending bit
- * order, one past the last = the relabelling schedule's out-of-place tile shape) with phase on (1) / off (0) / no butterflies at all (-1, a pure streaming copy of
- * the same access pattern), on the handle's stream; *ms_out = mean ms per launch. */
+/* Diagnostic micro-benchmark (modifies the state): time `reps` back-to-back launches of the tile
+ * pass over tile set `set` (0 = bits 0..11, 1.. = the run sets in ascending bit order) with phase
+ * on (1) / off (0), or, for phase < 0, a memory-pattern probe without butterflies (-1 copy, -2 read
+ * only, -3 write only), on the handle's stream; *ms_out = mean ms per launch.  The pass program is
+ * the one the schedules would use for that set (per-warp turning kernel where eligible). */
 int qsim_bench_pass(qsim_t *q, int set, int phase, int reps, double *ms_out);
 
 /* Number of kernels the library has launched on this handle (for bench reporting). */

@@ -29,7 +29,7 @@ for n in a.n:
                 try:
                     ms = Q.qsim_bench_pass(s.h, k, ph, a.reps)
                 except Q.QsimError:
-                    break  # past the last set (the tile-major shape exists only with QSIM_TILEMAJOR=1)
+                    break  # past the last set
                 fac = 0.5 if ph in (-2, -3) else 1.0  # read-only / write-only move half the bytes
                 print(f"n={n} set={k} phase={ph} {ms:.3f} ms  ({fac * ideal / ms * 100:.1f}% of measured HBM peak)",
                       flush=True)
