@@ -576,7 +576,7 @@ def main():
                          "pass_share_of_step": pass_ms_max / ms_max,
                          "per_pass_program": per_kind, "algorithmic_1pass": alg},
             "extra_configs": extras,
-            "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")} if cpu else None),
+            "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "host")} if cpu else None),
             "e2e": {"value": (1 << n) * p / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "sec_per_step": e2e_s},
             "gpu_launches": int(launches),
