@@ -19,8 +19,11 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libqsim.so")
 LIB_DEBUG = os.path.join(HERE, "libqsim_debug.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("qsim_device.cu", "qsim_tma.cu", "qsim_extra.cu", "qsim_comm.cu", "qsim_engine.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("qsim_device.h", "qsim_kernels.cuh", "qsim_comm.h")] + [
+SOURCES = [os.path.join(CSRC, f) for f in ("qsim_tma_f32.cu", "qsim_tma_f64mv.cu", "qsim_tma_f64.cu", "qsim_tma_pw.cu",
+                                            "qsim_tma.cu", "qsim_device.cu", "qsim_extra.cu", "qsim_comm.cu",
+                                            "qsim_engine.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("qsim_device.h", "qsim_kernels.cuh", "qsim_comm.h",
+                                                  "qsim_tma_impl.cuh")] + [
     os.path.join(ROOT, "include", "qsim.h"), os.path.abspath(__file__)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
