@@ -146,3 +146,35 @@ def test_loopback_stg_moves(world, n, inplace, monkeypatch):
     if inplace:
         monkeypatch.setenv("QSIM_SWAP_INPLACE", "1")
     _check(world, n, Q.QSIM_SWAP_FUSED_INPLACE if inplace else Q.QSIM_SWAP_FUSED_SPLIT, extras=False)
+
+
+def test_loopback_caller_owned_buffers():
+    """state_buf on a sharded handle: no fused swap (its peer mappings need library-owned
+    buffers), so the ranks take the collective swap; parity against the oracle."""
+    import numpy as np
+    import torch
+
+    from oracle import oracle as o
+    from paper_2104_03293_b200 import instances as inst
+
+    Q = _q()
+    n, world = 20, 2
+    h, J = inst.random_ising(n, 62)
+    g, b = np.array([0.4, -0.3, 0.7]), np.array([0.5, -0.6, 1.2])
+    bufs = [torch.zeros(1 << (n - 1), dtype=torch.complex128, device="cuda") for _ in range(world)]
+
+    def body(rank, _new_sim):
+        s = Q.QSim(n, rank=rank, world=world, nccl_unique_id=ids, state_buf=bufs[rank].data_ptr(),
+                   buf_bytes=bufs[rank].numel() * 16)
+        try:
+            s.set_ising(h, J)
+            s.init_plus()
+            s.apply_qaoa(g, b)
+            return s.amplitudes(), s.swap_path
+        finally:
+            s.close()
+
+    ids = Q.qsim_loopback_id(world)
+    psi, path = run_loopback(world, body)
+    assert path == Q.QSIM_SWAP_COLLECTIVE
+    assert np.max(np.abs(psi - o.qaoa_state(h, J, g, b))) <= 1e-10

@@ -674,3 +674,29 @@ def test_qaoa_batch_needs_small_state(Q):
         with pytest.raises(Q.QsimError) as ei:
             s.qaoa_batch([[0.1]], [[0.2]])
         assert ei.value.code == Q.QSIM_EUNSUPPORTED
+
+
+# ------------------------------------------------------------------ caller-owned state buffer
+def test_caller_owned_state_buffer(Q):
+    """qsim_create_ex with state_buf: the library computes in the caller's device memory (here a
+    torch tensor) and never frees it; with |tan beta| < 1 no index flips occur, so the tensor holds
+    the amplitudes in logical order after the call."""
+    import torch
+
+    n = 20
+    h, J = inst.random_ising(n, 61)
+    g, b = np.array([0.4, -0.3]), np.array([0.5, -0.6])
+    buf = torch.zeros(1 << n, dtype=torch.complex128, device="cuda")
+    st = torch.cuda.current_stream()
+    with Q.QSim(n, state_buf=buf.data_ptr(), buf_bytes=buf.numel() * 16, cuda_stream=st.cuda_stream) as s:
+        s.set_ising(h, J)
+        s.init_plus()
+        s.apply_qaoa(g, b)
+        psi = s.amplitudes()
+    ref = o.qaoa_state(h, J, g, b)
+    assert_state_close(psi, ref)
+    torch.cuda.synchronize()
+    assert np.max(np.abs(buf.cpu().numpy() - ref)) <= AMP_TOL
+    with pytest.raises(Q.QsimError) as ei:  # too small a buffer is EINVAL
+        Q.QSim(n, state_buf=buf.data_ptr(), buf_bytes=buf.numel() * 8, cuda_stream=st.cuda_stream)
+    assert ei.value.code == Q.QSIM_EINVAL
