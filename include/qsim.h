@@ -168,8 +168,10 @@ int qsim_success_prob(qsim_t *q, const uint64_t *ground_states, int count, doubl
  * relabelling done by the multi-GPU engine is undone) to out[2*count]. */
 int qsim_get_amplitudes(qsim_t *q, uint64_t first, uint64_t count, double *out);
 
-/* Test / diagnostic: E(z) for z = first .. first+count-1, computed on the device with
- * the same tile-factorised energy arithmetic the cost-phase kernel uses. */
+/* Test / diagnostic: E(z) for z = first .. first+count-1, computed on the device with the hot
+ * path's own arithmetic: the per-tile records of tile_fields_kernel (12-bit set) and the register
+ * tree of the reducing pass (frame Z), in the same summation order (for n <= 12 the small-state
+ * kernel's direct sum).  Multi-GPU: the rank owning each label computes it, the others add zero. */
 int qsim_energies(qsim_t *q, uint64_t first, uint64_t count, double *out);
 
 /* spin expectations <sigma^z_i> = sum_z |psi_z|^2 s_i(z), i = 0..n-1 in
