@@ -182,3 +182,36 @@ def test_profile_pass_codes_match_header(Q):
                  "QSIM_SWAP_INPLACE_STAGED", "QSIM_SWAP_COLLECTIVE", "QSIM_SWAP_LOWBIT", "QSIM_SWAP_FUSED_SPLIT"):
         m = re.search(name + r"\s*=\s*(\d+)", txt)
         assert m and int(m.group(1)) == getattr(Q, name), name
+
+
+def _build_c_example(tmpdir):
+    import subprocess
+
+    exe = os.path.join(str(tmpdir), "qaoa_c")
+    libdir = os.path.join(ROOT, "paper_2104_03293_b200")
+    subprocess.check_call(["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "qaoa_c.c"), "-L", libdir, "-l:libqsim.so",
+                           f"-Wl,-rpath,{libdir}", "-o", exe])
+    return exe
+
+
+def test_c_example_compiles_and_links(Q, tmp_path):
+    """examples/qaoa_c.c uses the C-ABI from plain C (no Python, no torch): it compiles against
+    include/qsim.h and links against libqsim.so (running it needs a GPU: test_gpu_parity)."""
+    assert os.path.exists(_build_c_example(tmp_path))
+
+
+def c_example_instance(n, p):
+    """the LCG instance and angles of examples/qaoa_c.c, reproduced for the oracle"""
+    seed = 12345
+    M = (1 << 64) - 1
+    h = np.zeros(n)
+    J = np.zeros((n, n))
+    for i in range(n):
+        seed = (seed * 6364136223846793005 + 1442695040888963407) & M
+        h[i] = (int((seed >> 33) % 9) - 4) / 2.0
+        for j in range(i + 1, n):
+            seed = (seed * 6364136223846793005 + 1442695040888963407) & M
+            J[i, j] = (int((seed >> 33) % 5) - 2) / 2.0
+    k = np.arange(1, p + 1)
+    return h, J, 0.8 * k / (p + 1), -0.6 * (1.0 - k / (p + 1))

@@ -700,3 +700,24 @@ def test_caller_owned_state_buffer(Q):
     with pytest.raises(Q.QsimError) as ei:  # too small a buffer is EINVAL
         Q.QSim(n, state_buf=buf.data_ptr(), buf_bytes=buf.numel() * 8, cuda_stream=st.cuda_stream)
     assert ei.value.code == Q.QSIM_EINVAL
+
+
+def test_c_example_runs_against_oracle(Q, tmp_path):
+    """examples/qaoa_c.c (the C-ABI from plain C) on the GPU: its <H_C>, norm and ground-state energy
+    against the oracle on the same instance."""
+    import re
+    import subprocess
+
+    from tests.test_abi_host import _build_c_example, c_example_instance
+
+    exe = _build_c_example(tmp_path)
+    n, p = 18, 3
+    out = subprocess.run([exe, str(n), str(p)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    m = re.search(r"<H_C>=(\S+) norm=(\S+) .* E_min=(\S+) minimisers=(\d+)", out.stdout)
+    assert m, out.stdout
+    h, J, g, b = c_example_instance(n, p)
+    ref = o.qaoa_state(h, J, g, b)
+    assert_expect_close(float(m.group(1)), h, J, ref)
+    gs, emin, cnt = o.ground_states(h, J)
+    assert float(m.group(3)) == emin and int(m.group(4)) == cnt
