@@ -178,3 +178,17 @@ def test_loopback_caller_owned_buffers():
     psi, path = run_loopback(world, body)
     assert path == Q.QSIM_SWAP_COLLECTIVE
     assert np.max(np.abs(psi - o.qaoa_state(h, J, g, b))) <= 1e-10
+
+
+def test_loopback_create_errors():
+    """create-time validation of sharded handles: world must be a power of two <= 8 (EINVAL), the
+    shard must keep >= 15 local qubits (EUNSUPPORTED), and a group id serves exactly its world
+    (a loopback id made for 4 ranks is refused by a world-2 handle: ENCCL)."""
+    Q = _q()
+    uid4 = Q.qsim_loopback_id(4)
+    for args, code in [((20, 0, 3, uid4), Q.QSIM_EINVAL), ((15, 0, 2, Q.qsim_loopback_id(2)), Q.QSIM_EUNSUPPORTED),
+                       ((20, 0, 2, uid4), Q.QSIM_ENCCL), ((20, 2, 2, Q.qsim_loopback_id(2)), Q.QSIM_EINVAL)]:
+        n, rank, world, uid = args
+        with pytest.raises(Q.QsimError) as ei:
+            Q.QSim(n, rank=rank, world=world, nccl_unique_id=uid)
+        assert ei.value.code == code, (args, ei.value)
