@@ -48,6 +48,44 @@ __global__ void __launch_bounds__(256) probe(const double2 *__restrict__ in, dou
     }
 }
 
+// relabelling copy of the run slot R1 = {16..24}: tile id ut (bits = input positions 3..15, 25..29
+// ascending); the tile goes to positions 0..11, the home bits 3..11 to 16..24.  ROT rotates the
+// processing order so that tile-id bit ROT varies fastest (0: input position 3 first = adjacent
+// 128 B read rows, output tiles 1 MiB apart; 9: position 12 first = output tiles consecutive)
+template <int ROT>
+__global__ void __launch_bounds__(256) relabel_copy(const double2 *__restrict__ in, double2 *__restrict__ out) {
+    const u64 ntiles = 1ull << (N - 12);
+    for (u64 k = blockIdx.x; k < ntiles; k += gridDim.x) {
+        const u64 ut = ROT ? (((k << ROT) | (k >> (N - 12 - ROT))) & (ntiles - 1)) : k;
+        const u64 home = ut & 511, b12 = (ut >> 9) & 15, b25 = ut >> 13;
+        double2 v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const u64 e = (u64)threadIdx.x + 256ull * q;
+            v[q] = in[(e & 7) | (home << 3) | (b12 << 12) | ((e >> 3) << 16) | (b25 << 25)];
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const u64 e = (u64)threadIdx.x + 256ull * q;
+            out[e | (b12 << 12) | (home << 16) | (b25 << 25)] = make_double2(v[q].x * 1.0000001, v[q].y);
+        }
+    }
+}
+template <int ROT>
+float run_rl(double2 *a, double2 *b, int grid, int reps) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    relabel_copy<ROT><<<grid, 256>>>(a, b);
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) relabel_copy<ROT><<<grid, 256>>>(a, b);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return ms / reps;
+}
+
 template <int MODE>
 float run(double2 *a, double2 *b, int grid, int reps) {
     double2 *out = (MODE == 1 || MODE == 2) ? b : a;
@@ -87,6 +125,10 @@ int main() {
             const double by = (i >= 4 ? 1.0 : 2.0) * bytes;
             printf("grid %d x 256  %-30s %7.3f ms  %7.1f GB/s\n", grid, names[i], t[i], by / t[i] / 1e6);
         }
+        const float r0 = run_rl<0>(a, b, grid, 5), r9 = run_rl<9>(a, b, grid, 5), r13 = run_rl<13>(a, b, grid, 5);
+        printf("grid %d x 256  relabel copy, order home-first     %7.3f ms  %7.1f GB/s\n", grid, r0, 2.0 * bytes / r0 / 1e6);
+        printf("grid %d x 256  relabel copy, order pos-12-first   %7.3f ms  %7.1f GB/s\n", grid, r9, 2.0 * bytes / r9 / 1e6);
+        printf("grid %d x 256  relabel copy, order pos-25-first   %7.3f ms  %7.1f GB/s\n", grid, r13, 2.0 * bytes / r13 / 1e6);
     }
     cudaError_t e = cudaGetLastError();
     printf("%s\n", cudaGetErrorString(e));
