@@ -100,6 +100,11 @@ struct PassParams {
     // so that the tiles in flight at one time span all groups (moving passes interleave NVLink
     // and HBM traffic instead of alternating phases of each); 0 = natural order
     int ord_rot, ord_bits;
+    // spatial split of a whole-tile moving pass (mv 1, out of place): CTAs [0, sp_ctas) visit the
+    // moving tiles, the others the local ones, each stream in natural tile order (no group-bits-
+    // first rotation, which breaks the run sets' DRAM locality).  Tile id = low bits | group
+    // (sp_gpos, mv_pbits bits) | middle bits | destination rank (sp_dpos, gbits bits) | top bits.
+    int sp, sp_ctas, sp_gpos, sp_dpos;
     // e^{-i gamma E_RR(j ^ fr)} of the turning-run phase frame's 32 register patterns, computed on
     // the host (FP64 R_x turning-run passes of the single-GPU and top-bit schedules): read from
     // the constant bank instead of shared memory

@@ -390,6 +390,10 @@ struct qsim {
     bool res_valid = false;
     uint64_t launches = 0;
     int tma_store = 1;         // TMA stores from the stage (QSIM_TMA_STORE=0: STG from registers)
+    // spatial split of the whole-tile moving run passes (PassParams::sp): share of the CTAs on
+    // the moving tiles; >= 1 = the fraction of tiles that move, 0 = group-bits-first order
+    // instead (QSIM_SP)
+    double sp_frac = 1.0;
     std::string err;
     // optional per-pass timing (CUDA events on the handle's stream around each pass launch)
     bool prof = false;
@@ -934,11 +938,31 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
                 if (rc) return rc;
             }
             if (op.mv == 1 && P.mv_pbits > 0) {
-                // visit the tiles group bits first (the group bits are tile-id bits of every
-                // non-boundary set; their tile-id position = non-tile bits below them)
-                P.ord_bits = q->m - qk::KT;
+                // the group bits are tile-id bits of every non-boundary set; their tile-id position
+                // = non-tile bits below them
                 const int tpos = q->mv_pshift - __builtin_popcountll(S.lmask & ((1ull << q->mv_pshift) - 1ull));
-                P.ord_rot = tpos % P.ord_bits;
+                const int cb = q->m - q->g;
+                const int dpos = cb - __builtin_popcountll(S.lmask & ((1ull << cb) - 1ull));
+                const u64 fields = (((1ull << P.mv_pbits) - 1ull) << q->mv_pshift) | (((1ull << q->g) - 1ull) << cb);
+                const int grid = (int)std::min<u64>((u64)q->num_sms, S.ntiles);
+                if (!q->ipfused && !S.full12 && q->sp_frac > 0.0 && !(S.lmask & fields) && tpos + P.mv_pbits <= dpos && grid >= 2) {
+                    // spatial split: a share of the CTAs visits the moving tiles, the rest the
+                    // local ones, both in natural order.  Default share = the fraction of tiles
+                    // that move (a moving tile takes about as long as a local one at these
+                    // concurrencies); QSIM_SP=<share> overrides.  Measured optima on the run
+                    // pass: 0.18 at G = 2 (fraction 1/6), 0.25 at G = 4 (1/4); DESIGN §8
+                    P.sp = 1;
+                    P.sp_gpos = tpos;
+                    P.sp_dpos = dpos;
+                    const double G = (double)(1 << q->g);
+                    const double fm = (double)(op.hi - op.lo) * (G - 1.0) / ((double)(1 << P.mv_pbits) * G);
+                    const double share = q->sp_frac >= 1.0 ? fm : q->sp_frac;
+                    P.sp_ctas = std::max(1, std::min(grid - 1, (int)std::lround(share * grid)));
+                } else {
+                    // visit the tiles group bits first (moving and local tiles interleave in time)
+                    P.ord_bits = q->m - qk::KT;
+                    P.ord_rot = tpos % P.ord_bits;
+                }
             }
         }
         P.pw = pw_eligible(q, S, P);  // after the swap setup: moving passes keep the group kernel
@@ -1249,6 +1273,7 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     }
     q->pending_plus = true;
     if (const char *e = std::getenv("QSIM_TMA_STORE")) q->tma_store = std::atoi(e) != 0;
+    if (const char *e = std::getenv("QSIM_SP")) q->sp_frac = std::atof(e);
     if (const char *e = std::getenv("QSIM_TMA_MOVES")) q->tma_moves = std::atoi(e) != 0;
 
 

@@ -191,10 +191,64 @@ __device__ __forceinline__ void ip_wait_peers(const PassParams &P, int gt, int g
 // global sequence index of the CTA's i-th tile (cyclic over CTAs)
 __device__ __forceinline__ u64 seq_of(const PassParams &, u64 i) { return blockIdx.x + i * (u64)gridDim.x; }
 
+// ---- spatial split (PassParams::sp): combos (group, destination) of the moving stream are
+// grp in [mv_lo, mv_hi) x dest != rank; the local stream has the same groups with dest == rank,
+// then every other group with any dest.  Within a combo the remaining tile-id bits run fastest.
+__device__ __forceinline__ u64 sp_rest_bits(const PassParams &P) { return (u64)(P.m - KT - P.mv_pbits - P.gbits); }
+__device__ __forceinline__ u64 sp_count(const PassParams &P, bool moving) {
+    const u64 G = 1ull << P.gbits, ng = 1ull << P.mv_pbits, nm = (u64)(P.mv_hi - P.mv_lo) * (G - 1);
+    return (moving ? nm : ng * G - nm) << sp_rest_bits(P);
+}
+__device__ __forceinline__ u64 sp_tile(const PassParams &P, bool moving, u64 j) {
+    const u64 G = 1ull << P.gbits, span = (u64)(P.mv_hi - P.mv_lo);
+    const u64 c = j >> sp_rest_bits(P);
+    u64 r = j & ((1ull << sp_rest_bits(P)) - 1ull);
+    u64 grp, d;
+    if (moving) {
+        grp = P.mv_lo + c / (G - 1);
+        d = c % (G - 1);
+        if (d >= (u64)P.rank) ++d;
+    } else if (c < span) {
+        grp = P.mv_lo + c;
+        d = (u64)P.rank;
+    } else {
+        const u64 c2 = c - span, gi = c2 / G;
+        d = c2 % G;
+        grp = gi < P.mv_lo ? gi : gi + span;
+    }
+    const int gp = P.sp_gpos, ge = P.sp_gpos + P.mv_pbits, dp = P.sp_dpos;
+    const u64 lo = r & ((1ull << gp) - 1ull);
+    r >>= gp;
+    const u64 mid = r & ((1ull << (dp - ge)) - 1ull);
+    r >>= (dp - ge);
+    return lo | (grp << gp) | (mid << ge) | (d << dp) | (r << (dp + P.gbits));
+}
+// the CTA's tile count and its i-th tile id
+template <int MV>
+__device__ __forceinline__ u64 cta_ntiles(const PassParams &P) {
+    if (MV && P.sp) {
+        const bool mvs = (int)blockIdx.x < P.sp_ctas;
+        const u64 k = mvs ? (u64)blockIdx.x : (u64)(blockIdx.x - P.sp_ctas);
+        const u64 w = mvs ? (u64)P.sp_ctas : (u64)(gridDim.x - P.sp_ctas), cnt = sp_count(P, mvs);
+        return cnt > k ? (cnt - k + w - 1) / w : 0;
+    }
+    return (P.ntiles > blockIdx.x) ? (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+}
+template <int MV>
+__device__ __forceinline__ u64 cta_tile(const PassParams &P, u64 i) {
+    if (MV && P.sp) {
+        const bool mvs = (int)blockIdx.x < P.sp_ctas;
+        const u64 k = mvs ? (u64)blockIdx.x : (u64)(blockIdx.x - P.sp_ctas);
+        const u64 w = mvs ? (u64)P.sp_ctas : (u64)(gridDim.x - P.sp_ctas);
+        return sp_tile(P, mvs, k + i * w);
+    }
+    return tile_of<MV>(P, seq_of(P, i));
+}
+
 template <int MV>
 __device__ __forceinline__ void issue_tile(const PassParams &P, const TmaIssue &I, u64 i, int s, bool load_state,
                                            bool load_rec) {
-    const u64 ut = tile_of<MV>(P, seq_of(P, i));
+    const u64 ut = cta_tile<MV>(P, i);
     const uint32_t bytes = (load_state ? I.tile_bytes : 0u) + (load_rec ? (uint32_t)TILE_REC_BYTES : 0u);
     if (!bytes) {
         I.issued[s] = I.issued[s] + 1;
@@ -298,7 +352,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     const int n = P.n;
     const bool need_e = TURN || P.reduce;
     const bool load_state = !(TURN && P.init) && !(P.dbg & 2);
-    const u64 ntl = (P.ntiles > blockIdx.x) ? (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const u64 ntl = cta_ntiles<MV>(P);
     volatile int *issued = reinterpret_cast<volatile int *>(smem + TmaSmem::iss_off);
     const TmaIssue I{&tmap, MV ? &smap : &tmap, reinterpret_cast<const TileRec *>(P.rec), stages, (uint32_t)(TILE * sizeof(V)),
                      srec, full, issued};
@@ -373,7 +427,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     };
     for (u64 i = g; i < ntl; i += TMA_NG) {
         const int s = (int)(i % NSTAGE);
-        const u64 ut = tile_of<MV>(P, seq_of(P, i));
+        const u64 ut = cta_tile<MV>(P, i);
         const u64 tb = tile_base(P, ut);
         QSIM_DCHECK(ut < P.ntiles && (tb >> P.m) == 0 && (tb & P.lmask) == 0);
         V *sm = reinterpret_cast<V *>(stages + (size_t)s * SM_TILE_BYTES);
