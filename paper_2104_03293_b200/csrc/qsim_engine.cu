@@ -944,8 +944,10 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
                 const int cb = q->m - q->g;
                 const int dpos = cb - __builtin_popcountll(S.lmask & ((1ull << cb) - 1ull));
                 const u64 fields = (((1ull << P.mv_pbits) - 1ull) << q->mv_pshift) | (((1ull << q->g) - 1ull) << cb);
-                const int grid = (int)std::min<u64>((u64)q->num_sms, S.ntiles);
-                if (!q->ipfused && !S.full12 && q->sp_frac > 0.0 && !(S.lmask & fields) && tpos + P.mv_pbits <= dpos && grid >= 2) {
+                const int gmax = q->ipfused ? q->grid_cap : 0;  // as launch_pass sizes the grid
+                const int grid = (int)std::min<u64>((u64)(gmax > 0 ? gmax : q->num_sms), S.ntiles);
+                if (!q->ipfused && !S.full12 && q->sp_frac > 0.0 && !(S.lmask & fields) && tpos + P.mv_pbits <= dpos &&
+                    grid >= 2) {
                     // spatial split: a share of the CTAs visits the moving tiles, the rest the
                     // local ones, both in natural order.  Default share = the fraction of tiles
                     // that move (a moving tile takes about as long as a local one at these

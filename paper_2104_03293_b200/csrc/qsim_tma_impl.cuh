@@ -204,10 +204,9 @@ __device__ __forceinline__ u64 sp_tile(const PassParams &P, bool moving, u64 j) 
     const u64 c = j >> sp_rest_bits(P);
     u64 r = j & ((1ull << sp_rest_bits(P)) - 1ull);
     u64 grp, d;
-    if (moving) {
+    if (moving) {  // dest = rank ^ (c' + 1): a tile and its partner on the peer share j
         grp = P.mv_lo + c / (G - 1);
-        d = c % (G - 1);
-        if (d >= (u64)P.rank) ++d;
+        d = (u64)P.rank ^ (c % (G - 1) + 1);
     } else if (c < span) {
         grp = P.mv_lo + c;
         d = (u64)P.rank;
@@ -233,6 +232,18 @@ __device__ __forceinline__ u64 cta_ntiles(const PassParams &P) {
         return cnt > k ? (cnt - k + w - 1) / w : 0;
     }
     return (P.ntiles > blockIdx.x) ? (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+}
+// the handshake slot of the CTA's i-th tile (in-place swap): its visiting index, which a moving
+// tile shares with its partner on the destination rank
+template <int MV>
+__device__ __forceinline__ u64 cta_slot(const PassParams &P, u64 i) {
+    if (MV && P.sp) {
+        const bool mvs = (int)blockIdx.x < P.sp_ctas;
+        const u64 k = mvs ? (u64)blockIdx.x : (u64)(blockIdx.x - P.sp_ctas);
+        const u64 w = mvs ? (u64)P.sp_ctas : (u64)(gridDim.x - P.sp_ctas);
+        return (mvs ? 0 : sp_count(P, true)) + k + i * w;
+    }
+    return seq_of(P, i);
 }
 template <int MV>
 __device__ __forceinline__ u64 cta_tile(const PassParams &P, u64 i) {
@@ -433,7 +444,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         V *sm = reinterpret_cast<V *>(stages + (size_t)s * SM_TILE_BYTES);
         const TileRec *R = srec + s;
         if (load_state || need_e) wait_tile(I, i);
-        if (MV && P.ip && gt == 0) ip_signal_tile(P, tb, seq_of(P, i));
+        if (MV && P.ip && gt == 0) ip_signal_tile(P, tb, cta_slot<MV>(P, i));
         // ------------------------------------------------ compact turning-run body
         // (instruction-cache footprint: one copy of the butterflies, the smem sweeps and the
         // phase, driven by four mix steps X(mix1) W(mix1) [phase] W(mix2) X(mix2))
@@ -495,7 +506,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                 }
                 store_lowswap<FX>(v, P, tb + offX, 0);
             } else if (MV && P.swap_store) {
-                if (P.ip) ip_wait_peers(P, gt, g, seq_of(P, i));
+                if (P.ip) ip_wait_peers(P, gt, g, cta_slot<MV>(P, i));
                 store_tile_swapped<FX>(v, P, tb + offX);
             } else if (P.tma_store) {
                 sts_frame<FX>(v, sm, lane, warp);
@@ -571,7 +582,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         if (TURN) {
             MIXF(FX, P.mix2 & TMX, 2);
             if (MV && P.swap_store) {
-                if (P.ip) ip_wait_peers(P, gt, g, seq_of(P, i));
+                if (P.ip) ip_wait_peers(P, gt, g, cta_slot<MV>(P, i));
                 store_tile_swapped<FX>(v, P, tb + offX);
             } else if (tstore) {
                 sts_frame<FX>(v, sm, lane, warp);
@@ -623,7 +634,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                         group_bar(g);
                         if (gt == 0) {
                             if (P.ip) {
-                                ip_wait(P, (int)vr, seq_of(P, i));
+                                ip_wait(P, (int)vr, cta_slot<MV>(P, i));
                                 asm volatile("fence.proxy.async.global;" ::: "memory");
                             }
                             const u64 cm = ((1ull << P.gbits) - 1ull) << P.chunk_cp;
@@ -643,7 +654,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
                         if (gt == 0 && i + NSTAGE < ntl)
                             issue_tile<MV>(P, I, i + NSTAGE, s, load_state, need_e);
                     }
-                    if (P.ip) ip_wait_peers(P, gt, g, seq_of(P, i), (int)vr);
+                    if (P.ip) ip_wait_peers(P, gt, g, cta_slot<MV>(P, i), (int)vr);
                     const u64 wm = ((1ull << P.gbits) - 1ull) << sh;
                     QSIM_DCHECK(((((tb & ~wm) | ((u64)P.rank << sh)) + offS) >> P.m) == 0);
                     store_tile<RUN ? FRN : FZ>(v, reinterpret_cast<V *>(P.dst[vr]) + ((tb & ~wm) | ((u64)P.rank << sh)) + offS,

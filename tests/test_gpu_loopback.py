@@ -5,7 +5,7 @@ stores, the split-swap group ranges, the in-place handshake and the permutation 
 bookkeeping are the NCCL path's; only the transport differs.  Every swap path runs here: fused
 split (default), fused in place (QSIM_SWAP_INPLACE=1: no second buffer, the n = 36 path),
 collective (QSIM_FUSED_SWAP=0), staged in place (both), low-bit (QSIM_LOWSWAP=1) and
-non-default split weights (QSIM_SPLIT_W), against the oracle (full state at n <= 24, structured
+non-default split weights (QSIM_SPLIT_W) and spatial-split shares (QSIM_SP), against the oracle (full state at n <= 24, structured
 pins P4/P8/P9 at n = 31-33, up to 8 ranks)."""
 from __future__ import annotations
 
@@ -112,6 +112,15 @@ def test_loopback_lowbit_swap(n, monkeypatch):
     Q = _q()
     monkeypatch.setenv("QSIM_LOWSWAP", "1")
     _check(2, n, Q.QSIM_SWAP_LOWBIT, p=4, extras=False)
+
+
+@pytest.mark.parametrize("world,n,sp", [(2, 22, "0"), (4, 24, "0"), (2, 24, "0.5"), (8, 23, "0.05")])
+def test_loopback_spatial_split_shares(world, n, sp, monkeypatch):
+    """QSIM_SP: the whole-tile moving run passes with the group-bits-first order (0) and with
+    non-default CTA shares for the moving tiles (the default share is covered above)."""
+    Q = _q()
+    monkeypatch.setenv("QSIM_SP", sp)
+    _check(world, n, Q.QSIM_SWAP_FUSED_SPLIT, extras=False)
 
 
 def test_loopback_split_weights(monkeypatch):
