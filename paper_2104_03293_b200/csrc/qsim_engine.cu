@@ -946,8 +946,11 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
                 const u64 fields = (((1ull << P.mv_pbits) - 1ull) << q->mv_pshift) | (((1ull << q->g) - 1ull) << cb);
                 const int gmax = q->ipfused ? q->grid_cap : 0;  // as launch_pass sizes the grid
                 const int grid = (int)std::min<u64>((u64)(gmax > 0 ? gmax : q->num_sms), S.ntiles);
-                if (!q->ipfused && !S.full12 && q->sp_frac > 0.0 && !(S.lmask & fields) && tpos + P.mv_pbits <= dpos &&
-                    grid >= 2) {
+                // (measured: helps on 2 GPUs at m = 30, 32 and on 4 at m = 30; hurts on 4 GPUs with four
+                // or more sets, m = 31: 54.3 -> 57.4-64.8 ms per layer at every share)
+                const bool sp_ok = !(q->world >= 4 && q->sets.size() >= 4);
+                if (sp_ok && !q->ipfused && !S.full12 && q->sp_frac > 0.0 && !(S.lmask & fields) &&
+                    tpos + P.mv_pbits <= dpos && grid >= 2) {
                     // spatial split: a share of the CTAs visits the moving tiles, the rest the
                     // local ones, both in natural order.  Default share = the fraction of tiles
                     // that move (a moving tile takes about as long as a local one at these
