@@ -607,8 +607,8 @@ int launch_pass(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, dou
     return QSIM_OK;
 }
 
-// the per-warp turning-run kernel (tma_turn_pw_kernel): FP64, R_x mixers, a run set of 3 or 5
-// passengers (9- or 7-bit run; the passenger box is 128 bytes: the SWIZZLE_128B span), mix2 = the
+// the per-warp turning-run kernel (tma_turn_pw_kernel): FP64, R_x mixers, a run set of 3..11
+// passengers (the innermost box is 128 bytes: the SWIZZLE_128B span), mix2 = the
 // whole run, mix1 = the whole run, nothing (init) or the top g run bits (a multi-GPU boundary
 // pass's arrivals), no fused reduction, no swap stores (any world: non-moving passes only).
 // Returns P.pw (0 = not eligible).  QSIM_TURN_PW=0 selects the group-synchronous kernel instead.
@@ -617,7 +617,7 @@ int pw_eligible(const qsim *q, const TileSet &S, const qk::PassParams &P) {
     if (off || q->f32 || P.gmix || P.kind != qk::K_TURN_RUN || P.reduce || P.mv || P.multi == 2) return 0;
     int np = 0;
     while (np < qk::KT && S.L[np] == np && !((S.own >> np) & 1u)) ++np;
-    if ((np != 3 && np != 5) || S.full12 || S.own != (((1u << (qk::KT - np)) - 1u) << np) || S.tm_box[0] != 16)
+    if (np < 3 || np > 11 || S.full12 || S.own != (((1u << (qk::KT - np)) - 1u) << np) || S.tm_box[0] != 16)
         return 0;
     if (P.mix2 != S.own) return 0;
     int m1 = -1;
@@ -625,7 +625,7 @@ int pw_eligible(const qsim *q, const TileSet &S, const qk::PassParams &P) {
     for (int g = 1; g <= 3 && m1 < 0; ++g)
         if (P.mix1 == (((1u << g) - 1u) << (qk::KT - g))) m1 = g;
     if (m1 < 0 || (m1 > 0 && np != 5)) return 0;  // arrivals-only mix1 occurs on 7-bit runs (>= 4 sets)
-    return 1 | ((np == 5) << 1) | (m1 << 2);
+    return 1 | (m1 << 2) | (np << 4);
 }
 
 // tensor maps of set S over every rank's destination buffer of a whole-tile moving pass

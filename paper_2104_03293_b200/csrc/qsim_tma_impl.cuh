@@ -758,23 +758,31 @@ struct PwSmem {
     static constexpr size_t total = TmaSmem::total + align;
 };
 
-// NP: passengers (3: 9-bit run, frames A + B; 5: 7-bit run, frames A + B5).  M1: mix1 = the whole
-// run (0; nothing on the write-only init pass) or only the top M1 run bits (the arriving global
-// qubits of a multi-GPU boundary pass: frame A alone, one frame change fewer)
+// NP: passengers, run = tile bits NP..11.  Frame A (registers t7..t11) holds the top of every
+// run; the run bits below t7 are mixed in frame B (registers t3..t7: mask of t_NP..t6) or, for
+// NP = 5, in frame B5 (registers t5..t9).  NP >= 7: the whole run is in frame A's registers (no
+// frame change at all).  M1: mix1 = the whole run (0; nothing on the write-only init pass) or only
+// the top M1 run bits (the arriving global qubits of a multi-GPU boundary pass: frame A alone, one
+// frame change fewer; NP = 5)
+template <int NP>
+struct PwMasks {
+    static constexpr bool AONLY = NP >= 7;
+    static constexpr unsigned B = NP == 5 ? 0x03u : ((0x0Fu << (NP - 3)) & 0x0Fu);  // frame B(5) slots
+    static constexpr unsigned A = AONLY ? ((0x1Fu << (NP - 7)) & 0x1Fu) : 0x1Fu;    // frame A slots
+};
 template <int NP, int M1>
 __device__ __forceinline__ void pw_ldsB(double2 (&v)[NR], const double2 *sm, int baseB) {
-    if (NP == 3) lds_pwB(v, sm, baseB);
-    else lds_pwB5(v, sm, baseB);
+    if (NP == 5) lds_pwB5(v, sm, baseB);
+    else lds_pwB(v, sm, baseB);
 }
 template <int NP, int M1>
 __device__ __forceinline__ void pw_stsB(const double2 (&v)[NR], double2 *sm, int baseB) {
-    if (NP == 3) sts_pwB(v, sm, baseB);
-    else sts_pwB5(v, sm, baseB);
+    if (NP == 5) sts_pwB5(v, sm, baseB);
+    else sts_pwB(v, sm, baseB);
 }
 template <int NP>
 __device__ __forceinline__ void pw_mixB(double2 (&v)[NR], double t) {
-    if (NP == 3) stages_c<0x0Fu>(v, RxStage{t});  // t3..t6
-    else stages_c<0x03u>(v, RxStage{t});          // t5, t6
+    stages_c<PwMasks<NP>::B>(v, RxStage{t});  // NP = 3: t3..t6, 4: t4..t6, 6: t6, 5 (B5): t5, t6
 }
 
 template <int NP, int M1>
@@ -819,7 +827,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     }
     const int skB = frame_skew<FB, double2>(lane);
     const int baseA = swz128(Frame<FA>::tthr(lane, wi));
-    const int baseB = NP == 3 ? (Frame<FB>::tthr(lane, wi) ^ skB ^ (skB << 3))
+    const int baseB = NP != 5 ? (Frame<FB>::tthr(lane, wi) ^ skB ^ (skB << 3))
                               : (Frame<FB5>::tthr(lane, wi) ^ ((lane >> 1) & 3));
     __syncthreads();
 
@@ -835,7 +843,7 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         // slower: 6.54 -> 7.3 ms; the store's smem read completes late, so its wait stalls warp 0)
         wait_tile(I, i);
         if (load_state) {
-            if (M1 == 0) pw_ldsB<NP, M1>(v, sm, baseB);
+            if (M1 == 0 && !PwMasks<NP>::AONLY) pw_ldsB<NP, M1>(v, sm, baseB);
             else lds_pwA(v, sm, baseA);
         } else {
 #pragma unroll
@@ -848,7 +856,9 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             pend = -1;
         }
         if (load_state) {  // mix1 as the engine checked: the whole run, or the M1 arriving bits
-            if (M1 == 0) {
+            if (M1 == 0 && PwMasks<NP>::AONLY) {
+                stages_c<PwMasks<NP>::A>(v, RxStage{P.c1.t});
+            } else if (M1 == 0) {
                 pw_mixB<NP>(v, P.c1.t);
                 pw_stsB<NP, M1>(v, sm, baseB);
                 __syncwarp();
@@ -864,12 +874,16 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
             for (int r = 0; r < 5; ++r) uu[r] = uc[r * TMA_NG * 128 + tid];
             apply_phase<FA>(v, R, tE, fr, uc[5 * TMA_NG * 128 + tid], uu, P.PRR, nullptr, 0);
         }
-        stages_c<0x1Fu>(v, RxStage{P.c2.t});
-        sts_pwA(v, sm, baseA);
-        __syncwarp();
-        pw_ldsB<NP, M1>(v, sm, baseB);
-        pw_mixB<NP>(v, P.c2.t);
-        pw_stsB<NP, M1>(v, sm, baseB);
+        stages_c<PwMasks<NP>::A>(v, RxStage{P.c2.t});
+        if constexpr (PwMasks<NP>::AONLY) {
+            sts_pwA(v, sm, baseA);
+        } else {
+            sts_pwA(v, sm, baseA);
+            __syncwarp();
+            pw_ldsB<NP, M1>(v, sm, baseB);
+            pw_mixB<NP>(v, P.c2.t);
+            pw_stsB<NP, M1>(v, sm, baseB);
+        }
         // (re-reading the tile in frame X, releasing the stage at once and storing from registers
         // was measured slower: 6.5 -> 7.0-7.2 ms)
         fence_async_smem();
