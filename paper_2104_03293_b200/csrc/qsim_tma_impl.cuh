@@ -444,6 +444,9 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         V *sm = reinterpret_cast<V *>(stages + (size_t)s * SM_TILE_BYTES);
         const TileRec *R = srec + s;
         if (load_state || need_e) wait_tile(I, i);
+        // the deferred refill as soon as this tile is in, before its first frame load (after it:
+        // 12-bit pass 5.45 -> 5.40 ms, plain run 6.80 -> 6.66 in the bench step)
+        refill_pending();
         if (MV && P.ip && gt == 0) ip_signal_tile(P, tb, cta_slot<MV>(P, i));
         // ------------------------------------------------ compact turning-run body
         // (instruction-cache footprint: one copy of the butterflies, the smem sweeps and the
@@ -842,18 +845,20 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
         // (refilling the previous stage before this wait when the tile is not in yet was measured
         // slower: 6.54 -> 7.3 ms; the store's smem read completes late, so its wait stalls warp 0)
         wait_tile(I, i);
+        // deferred refill of the group's previous stage, as soon as this tile is in and before its
+        // first frame load (after the load: 7.05-7.08 ms per turning pass in the bench step, here
+        // 6.91; a TMA L2 prefetch of the tile 1-3 refills ahead was measured slower: 6.5 -> 7.4-8.3)
+        if (gt == 0 && pend >= 0) {
+            bulk_wait_read0();
+            if ((u64)pend + NSTAGE < ntl) issue_tile<0>(P, I, (u64)pend + NSTAGE, pend_s, load_state, true);
+            pend = -1;
+        }
         if (load_state) {
             if (M1 == 0 && !PwMasks<NP>::AONLY) pw_ldsB<NP, M1>(v, sm, baseB);
             else lds_pwA(v, sm, baseA);
         } else {
 #pragma unroll
             for (int j = 0; j < NR; ++j) v[j] = make_double2(P.a0, 0.0);
-        }
-        if (gt == 0 && pend >= 0) {  // deferred refill of the group's previous stage
-            bulk_wait_read0();
-            if ((u64)pend + NSTAGE < ntl) issue_tile<0>(P, I, (u64)pend + NSTAGE, pend_s, load_state, true);
-            // (a TMA L2 prefetch of the tile 1-3 refills ahead was measured slower: 6.5 -> 7.4-8.3 ms)
-            pend = -1;
         }
         if (load_state) {  // mix1 as the engine checked: the whole run, or the M1 arriving bits
             if (M1 == 0 && PwMasks<NP>::AONLY) {
