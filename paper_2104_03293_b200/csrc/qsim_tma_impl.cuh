@@ -426,9 +426,9 @@ __global__ void __launch_bounds__(TMA_NG * 128, 1)
     V v[NR];
     long long pend = -1;  // tile whose TMA store still reads its stage (deferred refill)
     int pend_s = 0;
-    // deferred refill: the TMA store of the group's previous tile is left running and
-    // its stage is refilled after this tile's first frame load, so the elected thread does not
-    // stall its warp (and the group's next barrier) on the store
+    // deferred refill: the TMA store of the group's previous tile is left running and its stage
+    // is refilled once this group's next tile is in, so the elected thread does not stall its warp
+    // (and the group's next barrier) on the store
     auto refill_pending = [&]() {
         if (gt == 0 && pend >= 0) {
             bulk_wait_read0();
