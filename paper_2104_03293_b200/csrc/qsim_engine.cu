@@ -394,6 +394,12 @@ struct qsim {
     // the moving tiles; >= 1 = the fraction of tiles that move, 0 = group-bits-first order
     // instead (QSIM_SP)
     double sp_frac = 1.0;
+    // L2 promotion of the run sets' tensor maps when tiles are visited in natural order: 256 B,
+    // i.e. a 128-byte row also pulls the neighbouring tile's row, which the next CTA is loading
+    // at the same time (single GPU: turning pass 6.95 -> 6.81 ms; 2 GPUs, spatial split: plain run
+    // 6.45 -> 5.6 ms).  The 12-bit set (contiguous), the in-place swap path and group-bits-first
+    // orders keep 128 B (in place: 7.2 -> 7.9 ms with 256 B).  QSIM_L2PROMO=128 / 64 / 0 for A/B
+    CUtensorMapL2promotion l2promo_run = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     std::string err;
     // optional per-pass timing (CUDA events on the handle's stream around each pass launch)
     bool prof = false;
@@ -591,7 +597,9 @@ int launch_pass(qsim *q, const TileSet &S, qk::PassParams &P, int *grid_out, dou
             CUresult r = enc(&tm[k], dt, 5u, (void *)(k ? out : q->psi), S.tm_dim,
                              S.tm_stride + 1, S.tm_box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                              P.pw ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                             (S.full12 || q->ipfused || P.ord_rot) ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                                   : q->l2promo_run,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS)
                 return fail(q, QSIM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
         }
@@ -1279,6 +1287,13 @@ int create_common(qsim *q, int n, int precision, int rank, int world, const void
     q->pending_plus = true;
     if (const char *e = std::getenv("QSIM_TMA_STORE")) q->tma_store = std::atoi(e) != 0;
     if (const char *e = std::getenv("QSIM_SP")) q->sp_frac = std::atof(e);
+    if (const char *e = std::getenv("QSIM_L2PROMO")) {
+        const int v = std::atoi(e);
+        q->l2promo_run = v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                   : v == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                   : v == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                              : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    }
     if (const char *e = std::getenv("QSIM_TMA_MOVES")) q->tma_moves = std::atoi(e) != 0;
 
 
