@@ -310,12 +310,13 @@ def test_full_size_energies_all_labels(Q, big30):
         assert np.array_equal(big30.energies(first, CH), o.energies(h, J, first, CH)), first
 
 
-@pytest.mark.parametrize("env", [{"QSIM_TURN_PW": "0"}, {"QSIM_RUNSPLIT": "0"}])
+@pytest.mark.parametrize("env", [{"QSIM_TURN_PW": "0"}, {"QSIM_RUNSPLIT": "0"}, {"QSIM_L2PROMO": "128"}])
 def test_full_size_kernel_switches(Q, env, monkeypatch):
     """The documented switches of the single-GPU n = 30 path: QSIM_TURN_PW=0 runs the turning
     passes on the group-synchronous kernel instead of the per-warp one, QSIM_RUNSPLIT=0 uses
-    contiguous runs instead of the split-run layout; both against the p = 1 closed form (P4)
-    and the product-state amplitudes (P8) at p = 3."""
+    contiguous runs instead of the split-run layout, QSIM_L2PROMO=128 keeps 128-byte L2 promotion
+    on the run sets' tensor maps; each against the p = 1 closed form (P4) and the product-state
+    amplitudes (P8) at p = 3."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     n = 30
