@@ -955,8 +955,9 @@ int apply_layers(qsim *q, const double *gam, const double *bet, int p) {
                 const int gmax = q->ipfused ? q->grid_cap : 0;  // as launch_pass sizes the grid
                 const int grid = (int)std::min<u64>((u64)(gmax > 0 ? gmax : q->num_sms), S.ntiles);
                 // (measured: helps on 2 GPUs at m = 30, 32 and on 4 at m = 30; hurts on 4 GPUs with four
-                // or more sets, m = 31: 54.3 -> 57.4-64.8 ms per layer at every share)
-                const bool sp_ok = !(q->world >= 4 && q->sets.size() >= 4);
+                // or more sets, m = 31: 54.3 -> 57.4-64.8 ms per layer at every share, also with the
+                // 256-byte promotion; an explicit QSIM_SP share in (0, 1) still forces it there)
+                const bool sp_ok = !(q->world >= 4 && q->sets.size() >= 4) || (q->sp_frac > 0.0 && q->sp_frac < 1.0);
                 if (sp_ok && !q->ipfused && !S.full12 && q->sp_frac > 0.0 && !(S.lmask & fields) &&
                     tpos + P.mv_pbits <= dpos && grid >= 2) {
                     // spatial split: a share of the CTAs visits the moving tiles, the rest the
